@@ -1,0 +1,378 @@
+"""Benchmark of the single-pass reduction (BASELINE.json metric: 1-pass TSQR/Gram
+GB/s of X and % of roofline), one JSON line on rank 0.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--m M]
+  python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
+  python bench.py --impl reference            # the reference's CPU path (oracle port) on host cores
+
+A step = one TSQR pass over the job's X (BASELINE config C2 by default: m = 2^26 rows, n = 200, fp64,
+107 GB resident in HBM; X row-sharded evenly over the N GPUs = config C3, strong scaling), i.e. the
+leaf kernel + on-GPU combine tree (+ for N > 1 one NCCL all-gather of the factors and the ordered
+device combine).  Gram and GX (k = 400) passes over the same X are timed the same way and reported
+under "gram" / "sketch".  X (107 GB) is far larger than L2 (126 MB), so no L2 flush is needed.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAK_TFLOPS = 37.0  # measured DMMA peak, profiles/r01_peaks.json (no FP64 entry in MEASURED_PEAKS.json)
+METRIC = "1-pass TSQR/Gram GB/s of X and % of HBM peak at 1/2/4/8 B200 vs CPU ref"
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        return 6650.0, "fallback B200_PROFILING.md"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="C2")
+    p.add_argument("--m", type=int, default=None, help="override total rows")
+    p.add_argument("--k", type=int, default=400, help="sketch rows for the GX pass")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-extra", action="store_true", help="skip the Gram / GX passes")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+
+
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 7:
+                    rows.append(parts)
+        except Exception:
+            pass
+        finally:
+            if self.path and os.path.exists(self.path):
+                os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows),
+                "power_w_max": max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())}
+
+
+# ---------------------------------------------------------------------------
+# reference arm / CPU baseline: the oracle port of the reference's stream_pass on host cores
+
+
+def _cpu_worker(args):
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+
+    from oracle import tsnmf_oracle as o
+
+    spec_name, n_chunks, chunk_rows, seed, sketch, start_at = args
+    spec = o.config_spec(spec_name)
+    mix = o.config_mixing(spec)[0]
+    bufs = [o.config_rows(spec, i * chunk_rows, chunk_rows, mix) for i in range(2)]
+    while start_at and time.time() < start_at:  # all workers start the timed pass together
+        time.sleep(0.001)
+    with threadpool_limits(1):
+        t0 = time.perf_counter()
+        res = o.stream_pass(((i * chunk_rows, bufs[i % 2]) for i in range(n_chunks)),
+                            sketch_rows=sketch, seed=seed)
+        dt = time.perf_counter() - t0
+    return dt, res.rows, np.asarray(res.r)
+
+
+def cpu_reference(spec_name: str, n: int, seconds: float, sketch=None):
+    """Time the reference algorithm (oracle port: per-8192-row-chunk LAPACK QR + TreeReducer,
+    reference tsqr.py:276-343) with one process per host core on a bounded sample; the per-process
+    factors are combined with the reference TreeReducer(combine) (SURVEY.md §8d best-effort CPU)."""
+    import multiprocessing as mpc
+
+    from oracle import tsnmf_oracle as o
+
+    cores = len(os.sched_getaffinity(0))
+    chunk_rows = 8192
+    # calibrate: chunks on one core
+    probe = _cpu_worker((spec_name, 4, chunk_rows, 0, sketch, 0))[0] / 4
+    per_proc = max(2, int(seconds / max(probe, 1e-3)))
+    ctx = mpc.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        outs = pool.map(_cpu_worker, [(spec_name, per_proc, chunk_rows, 0, sketch, time.time() + 3.0)] * cores)
+    t0 = time.perf_counter()
+    red = o.TreeReducer(o.combine)
+    for _, _, r in outs:
+        red.push(r)
+    red.result()
+    wall = max(dt for dt, _, _ in outs) + (time.perf_counter() - t0)
+    rows = sum(r for _, r, _ in outs)
+    gbs = rows * n * 8 / wall / 1e9
+    return {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "port",
+            "sample": f"{rows} rows x {n} cols of {spec_name} ({cores} procs x {per_proc} chunks of {chunk_rows} "
+                      f"rows, numpy/OpenBLAS LAPACK QR per chunk + TreeReducer, 1 BLAS thread each; "
+                      f"time = slowest process + final combine)"
+                      + (f" + GX k={sketch}" if sketch else ""),
+            "seconds": wall}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import tsnmf_oracle as o
+
+    spec = o.config_spec(args.config)
+    steps = []
+    base = None
+    for _ in range(args.warmup + args.steps):
+        base = cpu_reference(args.config, spec.n, max(2.0, args.cpu_seconds / 4))
+        steps.append(base["value"])
+    vals = steps[args.warmup:] or steps
+    v = statistics.median(vals)
+    line = {"metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": base["seconds"] * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"{args.config}: TSQR pass, m={spec.m}, n={spec.n} (bounded CPU sample)"},
+            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": base["cores"], "kind": "port",
+                             "sample": base["sample"]},
+            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1402_6964_b200 as tb
+    from paper_1402_6964_b200 import _native, sharded, synthetic
+    from paper_1402_6964_b200 import device as dv
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    devc = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=devc)
+    lib = _native.load()
+
+    spec = synthetic.config(args.config)
+    if args.m:
+        spec = synthetic.config(args.config, m=args.m)
+    m, n = spec.m, spec.n
+    lo, hi = sharded.shard_range(m, world, rank)
+    x = torch.empty((hi - lo, n), dtype=torch.float64, device=devc)
+    mix = synthetic.mixing(spec)[0]
+    synthetic.generate_into(x, spec, row0=lo, mix=mix)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=devc)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def tsqr_step():
+        r, l1, sq = dv.tsqr(x, stats=True)
+        if world > 1:
+            part = sharded.ShardPartials(r=r, l1=l1, sumsq=sq, rows=hi - lo)
+            sharded.exchange(part, dv.combine_factors)
+        return r
+
+    def gram_step():
+        g, l1, sq = dv.gram(x, stats=True)
+        if world > 1:
+            dist.all_reduce(g)
+        return g
+
+    def sketch_step():
+        s = dv.sketch(x, lo, 0, args.k)
+        if world > 1:
+            dist.all_reduce(s)
+        return s
+
+    def timed(fn, steps, warmup, slot):
+        for _ in range(warmup):
+            fn()
+        barrier()
+        lib.tsnmf_profile_read(slot, None, None)  # drop warm-up events
+        lib.tsnmf_profile_enable(1)
+        launches0 = lib.tsnmf_launch_count()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            fn()
+        e1.record()
+        barrier()
+        lib.tsnmf_profile_enable(0)
+        launches = lib.tsnmf_launch_count() - launches0
+        ms = max_over_ranks(e0.elapsed_time(e1)) / steps
+        tot = np.zeros(1)
+        cnt = np.zeros(1, dtype=np.int64)
+        import ctypes
+
+        tms, tl = ctypes.c_double(), ctypes.c_longlong()
+        _native.check(lib.tsnmf_profile_read(slot, ctypes.byref(tms), ctypes.byref(tl)))
+        kern_ms = tms.value / max(tl.value, 1)
+        del tot, cnt
+        return ms, kern_ms, int(launches), int(tl.value)
+
+    hbm, hbm_src = hbm_peak()
+    bytes_total = m * n * 8
+    bytes_local = (hi - lo) * n * 8
+    with ClockSampler(local) as clk:
+        ms, leaf_ms, launches, _ = timed(tsqr_step, args.steps, args.warmup, 0)
+        # combine-tree share (same run, separate slot)
+    clocks = clk.summary()
+    value = bytes_total / (ms * 1e-3) / 1e9
+    leaf_flops = 2.0 * n * n * (hi - lo)
+    leaf_tf = leaf_flops / (leaf_ms * 1e-3) / 1e12
+    plan = dv.tsqr_plan(n, hi - lo)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: TSQR pass (leaf + on-GPU combine tree"
+                               f"{' + NCCL all-gather + ordered combine' if world > 1 else ''}), R + column l1/l2",
+                   "m": m, "n": n, "r": spec.r, "sigma": spec.sigma, "rows_per_gpu": hi - lo,
+                   "resident_gb_per_gpu": round(bytes_local / 1e9, 2), "parallelism": f"rows{world}",
+                   "l2": "inputs (>=13 GB per GPU) exceed the 126 MB L2; no flush needed",
+                   "tsqr_plan": plan},
+        "roofline": {"bound": "tensor", "achieved": leaf_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": leaf_tf / FP64_PEAK_TFLOPS, "traffic": None,
+                     "kernel": "tsqr_leaf_kernel (FP64 DMMA m8n8k4)",
+                     "algorithmic": f"2 n^2 = {2 * n * n} flop per row x {hi - lo} rows per launch",
+                     "peak_source": "measured FP64 DMMA peak, profiles/r01_peaks.json",
+                     "kernel_ms": leaf_ms, "share_of_step": leaf_ms / ms,
+                     "hbm_gbs": bytes_local / (leaf_ms * 1e-3) / 1e9,
+                     "hbm_frac": bytes_local / (leaf_ms * 1e-3) / 1e9 / hbm, "hbm_peak": hbm,
+                     "hbm_peak_source": hbm_src},
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+
+    if not args.no_extra:
+        gms, gk_ms, _, _ = timed(gram_step, max(2, args.steps), 1, 2)
+        gflops = 1.0 * n * (n + 1) * (hi - lo)
+        line["gram"] = {"value": bytes_total / (gms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": gms,
+                        "kernel_ms": gk_ms, "kernel_tflops": gflops / (gk_ms * 1e-3) / 1e12,
+                        "frac_fp64": gflops / (gk_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+                        "hbm_frac": bytes_local / (gk_ms * 1e-3) / 1e9 / hbm}
+        sms, sk_ms, _, _ = timed(sketch_step, 2, 1, 3)
+        sflops = 2.0 * args.k * n * (hi - lo)
+        line["sketch"] = {"value": bytes_total / (sms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": sms,
+                          "k": args.k, "kernel_ms": sk_ms, "kernel_tflops": sflops / (sk_ms * 1e-3) / 1e12,
+                          "frac_fp64_gemm_only": sflops / (sk_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+                          "normals_per_s": args.k * (hi - lo) / (sk_ms * 1e-3)}
+
+    # end to end through the public API from pinned host buffers (H2D inside the timed region)
+    if not args.no_e2e:
+        pool_rows = min(hi - lo, (4 << 30) // (8 * n))
+        host = torch.empty((pool_rows, n), dtype=torch.float64).pin_memory()
+        host.copy_(x[:pool_rows].cpu())
+        hnp = host.numpy()
+        chunk_rows = 1 << 16
+
+        def chunks():
+            off = lo
+            while off < hi:
+                take = min(chunk_rows, hi - off)
+                src = (off - lo) % pool_rows
+                take = min(take, pool_rows - src)
+                yield tb.RowChunk(off, hnp[src:src + take])
+                off += take
+
+        def e2e_step():
+            return tb.stream_pass(chunks())
+
+        e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        e_steps = 2
+        for _ in range(e_steps):
+            res = e2e_step()
+        barrier()
+        e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / e_steps)
+        line["e2e"] = {"value": bytes_total / (e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e_ms,
+                       "h2d_bytes_per_step": bytes_local, "d2h_bytes_per_step": (n * n + 2 * n) * 8,
+                       "api": "paper_1402_6964_b200.stream_pass over host RowChunks (65536 rows each)",
+                       "host_pool": f"{pool_rows} pinned rows cycled (QR cost is data-independent)",
+                       "steps": e_steps, "timer": "host wall clock around the API call, barrier on both sides"}
+        assert res.rows == hi - lo
+
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_reference(args.config, n, args.cpu_seconds)
+        line["cpu_baseline"].pop("seconds", None)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

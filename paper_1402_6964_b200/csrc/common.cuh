@@ -1,0 +1,156 @@
+// Shared device helpers for the tsnmf B200 kernels (sm_100a only).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "tsnmf_b200 is written for sm_100a (B200) only"
+#endif
+
+namespace tsnmf {
+
+// Status codes mirror reference pkg/src/tsnmf/errors.py:16-31 (exit codes).
+enum Status : int { kOk = 0, kUsage = 1, kData = 2, kNumerical = 3, kCuda = 4 };
+
+// Set the thread-local error message (capi.cu) and return the status.
+int set_error(int status, const char* fmt, ...);
+
+#define TSNMF_CUDA_CHECK(expr)                                                              \
+  do {                                                                                      \
+    cudaError_t _e = (expr);                                                                \
+    if (_e != cudaSuccess)                                                                  \
+      return ::tsnmf::set_error(::tsnmf::kCuda, "%s failed: %s", #expr, cudaGetErrorString(_e)); \
+  } while (0)
+
+// Every kernel launch is followed by this check; it also feeds the launch counter (tsnmf_launch_count).
+void note_launch();
+#define TSNMF_LAUNCH_CHECK()      \
+  do {                            \
+    ::tsnmf::note_launch();       \
+    TSNMF_CUDA_CHECK(cudaGetLastError()); \
+  } while (0)
+
+// Optional CUDA-event timing of the dominant kernels on their launching stream (tsnmf_profile_*).
+enum ProfSlot : int { kProfTsqrLeaf = 0, kProfTsqrTree = 1, kProfGram = 2, kProfSketch = 3, kProfSlots = 4 };
+void prof_mark(int slot, bool begin, cudaStream_t st);
+
+constexpr int kNumSMs = 148;  // B200; launch code queries the device, this is only a default
+
+// ---------------------------------------------------------------------------
+// FP64 tensor-core MMA: D(8x8) += A(8x4) * B(4x8).  Fragment layout (per lane l):
+//   A: row l/4, col l%4        B: row l%4, col l/4        C/D: row l/4, cols 2*(l%4) + {0,1}
+// On sm_100a this lowers to one DMMA.8x8x4 (measured 37.0 TF/s chip-wide, profiles/r01_peaks.json).
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+// ---------------------------------------------------------------------------
+// Counter-based RNG, value-compatible with reference pkg/src/tsnmf/_kernels.pyx:21-69
+// (integer part bit-exact; log/cos/sqrt are CUDA libdevice, within a few ulp of libm).
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ULL;
+constexpr double kTwoPi = 6.283185307179586476925286766559;
+constexpr double kInv2p53 = 1.0 / 9007199254740992.0;
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+// word(s, c) = mix(s + (c + 1) * gamma)   (_kernels.pyx:31-32)
+__host__ __device__ __forceinline__ uint64_t rng_word(uint64_t stream, uint64_t ctr) {
+  return mix64(stream + (ctr + 1) * kGamma);
+}
+
+// rng.py:33-35
+__host__ __device__ __forceinline__ uint64_t derive_stream(uint64_t seed, uint64_t tag) {
+  return mix64(seed ^ mix64(tag + kGamma));
+}
+
+__device__ __forceinline__ double rng_uniform(uint64_t stream, uint64_t ctr) {
+  return __dmul_rn((double)(rng_word(stream, ctr) >> 11), kInv2p53);
+}
+
+// Standard normal #j: uniforms at counters 2j, 2j+1, Box-Muller cosine branch (_kernels.pyx:49-69).
+__device__ __forceinline__ double rng_normal(uint64_t stream, uint64_t j) {
+  double u1 = __dmul_rn(__dadd_rn((double)(rng_word(stream, 2 * j) >> 11), 0.5), kInv2p53);
+  double u2 = __dmul_rn((double)(rng_word(stream, 2 * j + 1) >> 11), kInv2p53);
+  return __dmul_rn(sqrt(__dmul_rn(-2.0, log(u1))), cos(__dmul_rn(kTwoPi, u2)));
+}
+
+// Single-precision Box-Muller on the same counters (2j, 2j+1), used ONLY by the synthetic-data
+// generator (BASELINE.json configs need ~1e10 Gaussians per run; the sketch's G always uses the
+// fp64 rng_normal above).  Mirrored by oracle/tsnmf_oracle.py normal_block_f32.
+__device__ __forceinline__ float rng_normal_f32(uint64_t stream, uint64_t j) {
+  const float u1 = __fmul_rn(__fadd_rn((float)(rng_word(stream, 2 * j) >> 40), 0.5f), 5.9604644775390625e-08f);
+  const float u2 = __fmul_rn((float)(rng_word(stream, 2 * j + 1) >> 40), 5.9604644775390625e-08f);
+  return __fmul_rn(sqrtf(__fmul_rn(-2.0f, logf(u1))), cosf(__fmul_rn(6.2831855f, u2)));
+}
+
+// Stream tags (rng.py:20-23) plus the config-generator tags (>= 4).
+constexpr uint64_t kTagSketch = 0;
+constexpr uint64_t kTagCfgW = 4, kTagCfgNoise = 7;
+
+__host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
+__host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ __forceinline__ int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+// smallest stride >= cols with stride % 16 == 8 (doubles): conflict-free DMMA fragment loads
+// (lane l reads row l%4, col l/4) and 16-byte C-tile accesses (row l/4, col 2*(l%4)).
+__host__ __device__ __forceinline__ int smem_stride(int cols) {
+  int s = cols;
+  while (s % 16 != 8) ++s;
+  return s;
+}
+
+// cp.async helpers (LDGSTS): global -> shared without staging through registers.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// Stage rows [0, nrows) x cols [0, ncols) of a row-major global matrix into shared memory with
+// row stride lds; rows [nrows, rows_total) and cols [ncols, cols_total) are zero-filled.
+// All threads of the CTA participate.  Caller commits / waits.
+__device__ __forceinline__ void stage_rows(double* __restrict__ dst, int lds, const double* __restrict__ src,
+                                           int64_t ldsrc, int nrows, int ncols, int rows_total,
+                                           int cols_total, bool vec16) {
+  const int tid = threadIdx.x, nth = blockDim.x;
+  if (vec16) {
+    const int pairs = ncols >> 1;
+    for (int idx = tid; idx < nrows * pairs; idx += nth) {
+      int r = idx / pairs, c = (idx - r * pairs) * 2;
+      cp_async16(dst + (int64_t)r * lds + c, src + r * ldsrc + c);
+    }
+    if (ncols & 1)
+      for (int r = tid; r < nrows; r += nth) cp_async8(dst + (int64_t)r * lds + ncols - 1, src + r * ldsrc + ncols - 1);
+  } else {
+    for (int idx = tid; idx < nrows * ncols; idx += nth) {
+      int r = idx / ncols, c = idx - r * ncols;
+      cp_async8(dst + (int64_t)r * lds + c, src + r * ldsrc + c);
+    }
+  }
+  if (ncols < cols_total) {
+    const int pad = cols_total - ncols;
+    for (int idx = tid; idx < nrows * pad; idx += nth) {
+      int r = idx / pad, c = ncols + (idx - r * pad);
+      dst[(int64_t)r * lds + c] = 0.0;
+    }
+  }
+  for (int idx = tid; idx < (rows_total - nrows) * cols_total; idx += nth) {
+    int r = nrows + idx / cols_total, c = idx % cols_total;
+    dst[(int64_t)r * lds + c] = 0.0;
+  }
+}
+
+}  // namespace tsnmf

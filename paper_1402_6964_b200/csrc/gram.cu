@@ -1,0 +1,237 @@
+// Gram reduction G = X^T X (+ fused column l1; sum of squares = diag G).
+//
+// NEW relative to the reference (no Gram code there: reference pkg/src/tsnmf/tsqr.py:6 "The Gram
+// matrix is never formed"); its parity anchor is the reference invariant
+// ||R^T R - X^T X||_F <= 1e-10 ||X^T X||_F (reference SPEC.md:164) and a per-chunk X.T @ X oracle.
+//
+// Layout: G is computed in 16x16 "super-tiles" (2x2 DMMA 8x8 tiles) over the upper triangle only.
+// grid = (tile groups, row splits).  A CTA stages BR rows of X into shared memory (cp.async, double
+// buffered) and each warp accumulates its super-tiles in registers; every 4 rows is one DMMA k-step
+// whose A and B fragments are the same 4x8 slab pattern X[i + l%4][8*cb + l/4].  Per-CTA partials go
+// to the workspace and are summed in a fixed order (deterministic) by gram_reduce_kernel.
+#include "common.cuh"
+#include "internal.h"
+
+namespace tsnmf {
+
+constexpr int kGrThreads = 256;
+constexpr int kGrWarps = kGrThreads / 32;
+constexpr int kGrSpw = 6;                       // super-tiles per warp
+constexpr int kGrSpc = kGrWarps * kGrSpw;       // super-tiles per CTA (tile group)
+constexpr int kGrBr = 32;                       // rows per stage
+
+struct GrGeom {
+  int n, npad;  // npad = round_up(n, 16)
+  int lds;      // smem stride
+  int ns;       // super-blocks per side (npad / 16)
+  int nst;      // super-tiles in the upper triangle
+  int groups;   // tile groups
+  int64_t rows_per_split;
+};
+
+__host__ __device__ inline void st_coords(int idx, int ns, int* P, int* Q) {
+  // row-major enumeration of {(P, Q) : 0 <= P <= Q < ns}
+  int p = 0, rem = idx;
+  while (rem >= ns - p) {
+    rem -= ns - p;
+    ++p;
+  }
+  *P = p;
+  *Q = p + rem;
+}
+
+__global__ void __launch_bounds__(kGrThreads, 2)
+    gram_kernel(const double* __restrict__ x, int64_t m, int64_t ldx, GrGeom g, double* __restrict__ partial,
+                double* __restrict__ l1part) {
+  extern __shared__ __align__(16) double smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int group = blockIdx.x;
+  const int64_t split = blockIdx.y;
+  const int64_t rbeg = split * g.rows_per_split;
+  const int64_t rend = min64(m, rbeg + g.rows_per_split);
+  const int lds = g.lds;
+  double* buf[2] = {smem, smem + kGrBr * lds};
+  const bool vec16 = ((ldx & 1) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+
+  int stP[kGrSpw], stQ[kGrSpw];
+  bool stv[kGrSpw];
+#pragma unroll
+  for (int u = 0; u < kGrSpw; ++u) {
+    const int idx = group * kGrSpc + warp * kGrSpw + u;  // contiguous run: shared P fragments
+    stv[u] = idx < g.nst;
+    int P = 0, Q = 0;
+    if (stv[u]) st_coords(idx, g.ns, &P, &Q);
+    stP[u] = P;
+    stQ[u] = Q;
+  }
+  double acc[kGrSpw][4][2];
+#pragma unroll
+  for (int u = 0; u < kGrSpw; ++u)
+#pragma unroll
+    for (int t = 0; t < 4; ++t) acc[u][t][0] = acc[u][t][1] = 0.0;
+  double l1a[2] = {0.0, 0.0};
+  const bool do_l1 = (group == 0) && (l1part != nullptr);
+
+  const int64_t nstages = ceil_div(max64(rend - rbeg, 0), kGrBr);
+  if (nstages > 0) {
+    stage_rows(buf[0], lds, x + rbeg * ldx, ldx, (int)min64(kGrBr, rend - rbeg), g.n, kGrBr, g.npad, vec16);
+    cp_async_commit();
+  }
+  for (int64_t s = 0; s < nstages; ++s) {
+    if (s + 1 < nstages) {
+      const int64_t r0 = rbeg + (s + 1) * kGrBr;
+      stage_rows(buf[(s + 1) & 1], lds, x + r0 * ldx, ldx, (int)min64(kGrBr, rend - r0), g.n, kGrBr,
+                 g.npad, vec16);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* xs = buf[s & 1];
+    if (do_l1) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = tid + h * kGrThreads;
+        if (col < g.n) {
+          double a = l1a[h];
+#pragma unroll 8
+          for (int i = 0; i < kGrBr; ++i) a += fabs(xs[i * lds + col]);
+          l1a[h] = a;
+        }
+      }
+    }
+#pragma unroll 2
+    for (int i = 0; i < kGrBr; i += 4) {
+      const double* row = xs + (i + (lane & 3)) * lds + (lane >> 2);
+#pragma unroll
+      for (int u = 0; u < kGrSpw; ++u) {
+        if (!stv[u]) continue;
+        const int P = stP[u], Q = stQ[u];
+        const double a0 = row[16 * P], a1 = row[16 * P + 8];
+        const double b0 = row[16 * Q], b1 = row[16 * Q + 8];
+        dmma(acc[u][0][0], acc[u][0][1], a0, b0);
+        dmma(acc[u][1][0], acc[u][1][1], a0, b1);
+        dmma(acc[u][3][0], acc[u][3][1], a1, b1);
+        if (P != Q) dmma(acc[u][2][0], acc[u][2][1], a1, b0);
+      }
+    }
+    __syncthreads();  // buffer reuse
+  }
+  // partial layout: [split][supertile][16][16]
+#pragma unroll
+  for (int u = 0; u < kGrSpw; ++u) {
+    if (!stv[u]) continue;
+    const int idx = group * kGrSpc + warp * kGrSpw + u;
+    double* dst = partial + (split * g.nst + idx) * 256;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int ti = t >> 1, tj = t & 1;
+      const int row = 8 * ti + (lane >> 2), col = 8 * tj + 2 * (lane & 3);
+      dst[row * 16 + col] = acc[u][t][0];
+      dst[row * 16 + col + 1] = acc[u][t][1];
+    }
+  }
+  if (do_l1) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int col = tid + h * kGrThreads;
+      if (col < g.npad) l1part[split * g.npad + col] = l1a[h];
+    }
+  }
+}
+
+__global__ void gram_reduce_kernel(const double* __restrict__ partial, int64_t splits, GrGeom g,
+                                   double* __restrict__ out, int64_t ldg, double* __restrict__ sumsq) {
+  const int i = blockIdx.x;  // output row
+  for (int j = i + threadIdx.x; j < g.n; j += blockDim.x) {
+    const int P = i / 16, Q = j / 16;
+    int idx = 0;
+    for (int p = 0; p < P; ++p) idx += g.ns - p;
+    idx += Q - P;
+    const int64_t off = (int64_t)idx * 256 + (i % 16) * 16 + (j % 16);
+    double acc = 0.0;
+    for (int64_t s = 0; s < splits; ++s) acc += partial[s * g.nst * 256 + off];
+    out[(int64_t)i * ldg + j] = acc;
+    out[(int64_t)j * ldg + i] = acc;
+    if (i == j && sumsq) sumsq[i] = acc;
+  }
+}
+
+__global__ void l1_reduce_kernel(const double* __restrict__ l1part, int64_t splits, int stride, int n,
+                                 double* __restrict__ l1) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double a = 0.0;
+  for (int64_t s = 0; s < splits; ++s) a += l1part[s * stride + j];
+  l1[j] = a;
+}
+
+namespace {
+
+GrGeom gr_geom(int64_t m, int n, int sms) {
+  GrGeom g;
+  g.n = n;
+  g.npad = (int)round_up(n, 16);
+  g.lds = smem_stride(g.npad);
+  g.ns = g.npad / 16;
+  g.nst = g.ns * (g.ns + 1) / 2;
+  g.groups = (int)ceil_div(g.nst, kGrSpc);
+  const int64_t target = max64(1, (int64_t)2 * sms / g.groups);
+  const int64_t splits = max64(1, min64(target, ceil_div(m, 4 * kGrBr)));
+  g.rows_per_split = round_up(ceil_div(m, splits), kGrBr);
+  return g;
+}
+
+size_t gr_smem(const GrGeom& g) { return sizeof(double) * 2 * kGrBr * (size_t)g.lds; }
+
+int64_t gr_splits(int64_t m, const GrGeom& g) { return max64(1, ceil_div(m, g.rows_per_split)); }
+
+int sm_count() {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = kNumSMs;
+  return sms;
+}
+
+}  // namespace
+
+int gram_max_cols() { return 512; }
+
+size_t gram_workspace_bytes(int64_t m, int n) {
+  if (n < 1 || n > gram_max_cols()) return 0;
+  GrGeom g = gr_geom(max64(m, 1), n, sm_count());
+  const int64_t splits = gr_splits(max64(m, 1), g);
+  return sizeof(double) * (size_t)(splits * g.nst * 256 + splits * g.npad) + 256;
+}
+
+int gram_run(const double* x, int64_t m, int n, int64_t ldx, double* gout, int64_t ldg, double* l1, double* sumsq,
+             void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (n > gram_max_cols()) return set_error(kUsage, "gram: n = %d exceeds %d", n, gram_max_cols());
+  GrGeom g = gr_geom(m, n, sm_count());
+  const int64_t splits = gr_splits(m, g);
+  const size_t need = sizeof(double) * (size_t)(splits * g.nst * 256 + splits * g.npad);
+  if (ws_bytes < need) return set_error(kUsage, "gram: workspace too small (%zu < %zu bytes)", ws_bytes, need);
+  double* partial = reinterpret_cast<double*>(ws);
+  double* l1part = partial + splits * g.nst * 256;
+  const size_t smem = gr_smem(g);
+  static bool attr = false;
+  if (!attr) {
+    TSNMF_CUDA_CHECK(cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+    attr = true;
+  }
+  prof_mark(kProfGram, true, st);
+  gram_kernel<<<dim3(g.groups, (unsigned)splits), kGrThreads, smem, st>>>(x, m, ldx, g, partial,
+                                                                         l1 ? l1part : nullptr);
+  TSNMF_LAUNCH_CHECK();
+  prof_mark(kProfGram, false, st);
+  gram_reduce_kernel<<<n, 128, 0, st>>>(partial, splits, g, gout, ldg, sumsq);
+  TSNMF_LAUNCH_CHECK();
+  if (l1) {
+    l1_reduce_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(l1part, splits, g.npad, n, l1);
+    TSNMF_LAUNCH_CHECK();
+  }
+  return kOk;
+}
+
+}  // namespace tsnmf

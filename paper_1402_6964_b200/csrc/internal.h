@@ -1,0 +1,43 @@
+// Internal (C++) entry points behind the C ABI in capi.cu.  All pointers are device pointers.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+namespace tsnmf {
+
+int set_error(int status, const char* fmt, ...);
+
+int tsqr_max_cols();
+size_t tsqr_workspace_bytes(int64_t m, int n);
+size_t combine_workspace_bytes(int count, int n);
+int tsqr_run(const double* x, int64_t m, int n, int64_t ldx, double* r, int64_t ldr, double* l1, double* sumsq,
+             void* ws, size_t ws_bytes, cudaStream_t st);
+int r_combine_run(const double* rs, int count, int n, double* r, int64_t ldr, void* ws, size_t ws_bytes,
+                  cudaStream_t st);
+int tsqr_describe(int n, int64_t m, int* nb, int* brows, int* ctas_per_sm, int* nleaves);
+
+int gram_max_cols();
+size_t gram_workspace_bytes(int64_t m, int n);
+int gram_run(const double* x, int64_t m, int n, int64_t ldx, double* g, int64_t ldg, double* l1, double* sumsq,
+             void* ws, size_t ws_bytes, cudaStream_t st);
+
+size_t sketch_workspace_bytes(int64_t m, int n, int k);
+int sketch_run(const double* x, int64_t m, int n, int64_t ldx, int64_t row_offset, uint64_t seed, int k,
+               const double* gexp, int64_t ldgexp, double* s, int64_t lds_out, void* ws, size_t ws_bytes,
+               cudaStream_t st);
+
+size_t stats_workspace_bytes(int64_t m, int n);
+int stats_run(const double* x, int64_t m, int n, int64_t ldx, double* l1, double* sumsq, void* ws, size_t ws_bytes,
+              cudaStream_t st);
+
+int uniform_block_run(uint64_t stream, uint64_t start, int64_t count, double* out, cudaStream_t st);
+int normal_block_run(uint64_t stream, uint64_t start, int64_t count, double* out, cudaStream_t st);
+int single_row_factor_run(const double* x, int n, double* r, int64_t ldr, cudaStream_t st);
+int generate_run(double* x, int64_t ldx, int64_t row0, int64_t rows, int n, int r, const double* mix, int w_kind,
+                 const double* bumps, int64_t m_total, double sigma, uint64_t seed, cudaStream_t st);
+
+}  // namespace tsnmf

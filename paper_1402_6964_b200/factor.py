@@ -1,0 +1,462 @@
+"""Single-pass TSQR / Gram reduction with fused column statistics — drop-in
+for reference pkg/src/tsnmf/tsqr.py (same names, signatures, result types and
+error behaviour), computed on the B200.
+
+Semantics kept from the reference:
+  * ``TriangularFactor`` / ``ColumnStats`` / ``ReducedSVD`` / ``StreamResult``
+    validation and read-only arrays (tsqr.py:27-110, 237-244);
+  * ``combine_order``: "tree" (binary-counter tree over the chunk index,
+    deterministic), "sequential" (left fold), "first-come" (accepted; on the
+    device the order is deterministic anyway) (tsqr.py:24, 294-333);
+  * errors: empty stream -> DataError, m < n -> DataError("not tall-and-skinny"),
+    bad order / threads -> UsageError (tsqr.py:294-297, 335-341).
+
+What changes: every chunk is reduced by ``libtsnmf_b200.so`` (device.py).
+Device-resident chunks (torch CUDA float64) are reduced in place; host chunks
+(numpy) are gathered into large pinned batches that stream over PCIe while the
+previous batch is being reduced.  ``threads`` is accepted for signature
+compatibility only.
+"""
+
+from __future__ import annotations
+
+import json
+from dataclasses import dataclass, field
+from pathlib import Path
+from typing import Iterable
+
+import numpy as np
+
+from . import device as dv
+from .errors import DataError, UsageError
+from .rowchunk import RowChunk
+
+COMBINE_ORDERS = ("tree", "sequential", "first-come")
+
+
+# ---------------------------------------------------------------------------
+# result types (reference tsqr.py:27-110)
+
+
+@dataclass(frozen=True)
+class TriangularFactor:
+    """n x n upper-triangular factor with a nonnegative diagonal (read-only)."""
+
+    entries: np.ndarray = field(repr=False)
+
+    def __post_init__(self):
+        e = self.entries
+        if e.ndim != 2 or e.shape[0] != e.shape[1]:
+            raise UsageError(f"triangular factor must be square, got {e.shape}")
+        if np.tril(e, -1).any():
+            raise UsageError("triangular factor has nonzero entries below the diagonal")
+        if (np.diagonal(e) < 0).any():
+            raise UsageError("triangular factor has a negative diagonal entry")
+        e.setflags(write=False)
+
+    @property
+    def n(self) -> int:
+        return self.entries.shape[0]
+
+    def save(self, path):
+        from .matio import write_matrix
+
+        write_matrix(path, self.entries)
+        Path(f"{path}.json").write_text(json.dumps({"kind": "triangular_factor", "n": self.n}, sort_keys=True))
+
+    @classmethod
+    def load(cls, path) -> "TriangularFactor":
+        from .matio import read_matrix
+
+        meta = json.loads(Path(f"{path}.json").read_text())
+        if meta.get("kind") != "triangular_factor":
+            raise DataError(f"{path} is not a saved triangular factor")
+        return cls(entries=read_matrix(path))
+
+
+@dataclass(frozen=True)
+class ColumnStats:
+    """Per-column l1 and l2 norms of the streamed matrix."""
+
+    l1: np.ndarray = field(repr=False)
+    l2: np.ndarray = field(repr=False)
+
+    def __post_init__(self):
+        self.l1.setflags(write=False)
+        self.l2.setflags(write=False)
+
+    @property
+    def n(self) -> int:
+        return self.l1.shape[0]
+
+    def norms(self, kind: str) -> np.ndarray:
+        if kind == "l1":
+            return self.l1
+        if kind == "l2":
+            return self.l2
+        raise UsageError(f"unknown norm kind {kind!r}")
+
+    def save(self, path):
+        from .matio import write_matrix
+
+        write_matrix(path, np.vstack([self.l1, self.l2]))
+        meta = {"kind": "column_stats", "n": self.n, "rows": ["l1", "l2"]}
+        Path(f"{path}.json").write_text(json.dumps(meta, sort_keys=True))
+
+    @classmethod
+    def load(cls, path) -> "ColumnStats":
+        from .matio import read_matrix
+
+        meta = json.loads(Path(f"{path}.json").read_text())
+        if meta.get("kind") != "column_stats":
+            raise DataError(f"{path} is not saved column stats")
+        both = read_matrix(path)
+        return cls(l1=both[0].copy(), l2=both[1].copy())
+
+
+@dataclass(frozen=True)
+class ReducedSVD:
+    singular_values: np.ndarray = field(repr=False)
+    right_vectors: np.ndarray = field(repr=False)
+
+    def reduced_matrix(self) -> np.ndarray:
+        """Sigma V^T: the n x n matrix handed to column selection."""
+        return self.singular_values[:, None] * self.right_vectors
+
+
+@dataclass(frozen=True)
+class StreamResult:
+    factor: TriangularFactor
+    stats: ColumnStats
+    sketch: object  # projection.SketchResult | None
+    rows: int
+    chunks: int
+    tree_depth: int
+
+
+@dataclass(frozen=True)
+class GramResult:
+    """NEW (no reference counterpart): X^T X and column norms from one pass."""
+
+    gram: np.ndarray = field(repr=False)
+    stats: ColumnStats
+    rows: int
+    chunks: int
+    tree_depth: int
+
+    def __post_init__(self):
+        self.gram.setflags(write=False)
+
+    def cholesky_factor(self) -> TriangularFactor:
+        """R = chol(X^T X) with the nonnegative-diagonal convention (raises
+        NumericalError when the Gram matrix is not numerically positive
+        definite).  Less stable than TSQR (error grows with cond(X)^2)."""
+        from .errors import NumericalError
+
+        try:
+            low = np.linalg.cholesky(self.gram)
+        except np.linalg.LinAlgError as exc:
+            raise NumericalError(f"Gram matrix not positive definite: {exc}") from exc
+        return TriangularFactor(entries=np.ascontiguousarray(low.T))
+
+
+# ---------------------------------------------------------------------------
+# small host-side helpers that the reference also keeps on the host
+
+
+def rsvd(r: TriangularFactor) -> ReducedSVD:
+    """SVD of the n x n factor (reference tsqr.py:156-160; LAPACK on host, n x n)."""
+    _, s, vt = np.linalg.svd(r.entries)
+    return ReducedSVD(singular_values=s, right_vectors=vt)
+
+
+def apply_column_scaling(r: TriangularFactor, stats: ColumnStats, norm_kind: str = "l1") -> TriangularFactor:
+    """R D^{-1}: the factor of the column-normalised data (reference tsqr.py:163-177)."""
+    norms = stats.norms(norm_kind)
+    if norms.shape != (r.n,):
+        raise UsageError("column stats do not match factor dimension")
+    bad = np.flatnonzero(norms <= 0.0)
+    if bad.size:
+        raise DataError(f"column {', '.join(str(int(j)) for j in bad)} has zero norm")
+    return TriangularFactor(entries=r.entries / norms)
+
+
+class TreeReducer:
+    """Binary-counter pairwise reduction (reference tsqr.py:201-234): pushing
+    items in index order reproduces a balanced tree; ``fn(older, newer)``."""
+
+    def __init__(self, combine_fn):
+        self._fn = combine_fn
+        self._levels: list = []
+
+    def push(self, item):
+        lvl = 0
+        while lvl < len(self._levels) and self._levels[lvl] is not None:
+            item = self._fn(self._levels[lvl], item)
+            self._levels[lvl] = None
+            lvl += 1
+        if lvl == len(self._levels):
+            self._levels.append(item)
+        else:
+            self._levels[lvl] = item
+
+    def result(self):
+        acc = None
+        for item in self._levels:
+            if item is not None:
+                acc = item if acc is None else self._fn(item, acc)
+        return acc
+
+    @property
+    def depth(self) -> int:
+        return len(self._levels)
+
+
+# ---------------------------------------------------------------------------
+# single-chunk entry points
+
+
+def _chunk_data(chunk):
+    return chunk.data if isinstance(chunk, RowChunk) else chunk
+
+
+def factor_chunk(chunk) -> TriangularFactor:
+    """Sign-fixed triangular factor of one row chunk (reference tsqr.py:129-141)."""
+    data = _chunk_data(chunk)
+    t = dv.torch()
+    if not isinstance(data, t.Tensor):
+        data = np.asarray(data, dtype=np.float64)
+    if data.ndim != 2 or data.shape[0] < 1:
+        raise UsageError(f"chunk must have at least one row, got shape {tuple(data.shape)}")
+    r, _, _ = dv.tsqr(data, stats=False)
+    return TriangularFactor(entries=r.cpu().numpy())
+
+
+def combine(r1: TriangularFactor, r2: TriangularFactor) -> TriangularFactor:
+    """Factor of the vertical stack [r1; r2] (reference tsqr.py:144-153)."""
+    if r1.n != r2.n:
+        raise UsageError(f"dimension mismatch: {r1.n} vs {r2.n}")
+    if not r1.entries.any():
+        return r2
+    if not r2.entries.any():
+        return r1
+    t = dv.torch()
+    dev = dv.require_device()
+    stack = t.from_numpy(np.stack([r1.entries, r2.entries])).to(dev)
+    return TriangularFactor(entries=dv.combine_factors(stack).cpu().numpy())
+
+
+# ---------------------------------------------------------------------------
+# the pass
+
+
+@dataclass
+class _Node:
+    r: object  # n x n device factor or None
+    l1: object
+    sq: object
+    sk: object  # k x n device sketch or None
+    g: object  # n x n device Gram or None
+    rows: int
+    n: int
+
+
+def _merge_nodes(a: _Node, b: _Node) -> _Node:
+    """merge_nodes of reference tsqr.py:307-311 on device tensors."""
+    if a.n != b.n:
+        raise UsageError(f"dimension mismatch: {a.n} vs {b.n}")
+    t = dv.torch()
+    r = dv.combine_factors(t.stack([a.r, b.r])) if a.r is not None else None
+    sk = None
+    if a.sk is not None:
+        if a.sk.shape != b.sk.shape:
+            raise UsageError(f"shape mismatch: {tuple(a.sk.shape)} vs {tuple(b.sk.shape)}")
+        sk = a.sk + b.sk
+    g = a.g + b.g if a.g is not None else None
+    return _Node(r, a.l1 + b.l1, a.sq + b.sq, sk, g, a.rows + b.rows, a.n)
+
+
+class _PassEngine:
+    """Reduces one device row block into a _Node with the requested outputs."""
+
+    def __init__(self, want_r: bool, sketch_rows, seed: int, want_gram: bool):
+        self.want_r, self.k, self.seed, self.want_gram = want_r, sketch_rows, seed, want_gram
+
+    def reduce(self, x, row_offset: int) -> _Node:
+        m, n = int(x.shape[0]), int(x.shape[1])
+        r = l1 = sq = g = sk = None
+        if self.want_r:
+            r, l1, sq = dv.tsqr(x, stats=True)
+        if self.want_gram:
+            g, gl1, gsq = dv.gram(x, stats=l1 is None)
+            if l1 is None:
+                l1, sq = gl1, gsq
+        if l1 is None:
+            l1, sq = dv.column_stats(x)
+        if self.k is not None:
+            sk = dv.sketch(x, row_offset, self.seed, self.k)
+        return _Node(r, l1, sq, sk, g, m, n)
+
+
+def _host_batches(chunks, batch_rows_for):
+    """Group consecutive host chunks whose rows are contiguous into batches.
+    Yields lists of (row_offset, array) pieces plus the number of input chunks
+    consumed.  Oversized chunks are split into batch-sized pieces."""
+    cur, cur_rows, cur_end, cur_n, consumed = [], 0, None, None, 0
+    for ch in chunks:
+        consumed += 1
+        data = np.asarray(ch.data, dtype=np.float64) if not _is_device(ch.data) else ch.data
+        if data.ndim != 2 or data.shape[0] < 1:
+            raise UsageError(f"chunk must have at least one row, got shape {tuple(data.shape)}")
+        n = data.shape[1]
+        cap = batch_rows_for(n)
+        off = int(ch.row_offset)
+        pos = 0
+        while pos < data.shape[0]:
+            if cur and (cur_end != off + pos or cur_n != n or cur_rows >= cap):
+                yield cur, consumed
+                consumed = 0
+                cur, cur_rows = [], 0
+            take = min(cap - cur_rows, data.shape[0] - pos)
+            cur.append((off + pos, data[pos:pos + take]))
+            cur_rows += take
+            cur_end, cur_n = off + pos + take, n
+            pos += take
+    if cur:
+        yield cur, consumed
+
+
+def _is_device(data) -> bool:
+    t = dv.torch()
+    return isinstance(data, t.Tensor) and data.is_cuda
+
+
+HOST_BATCH_BYTES = 1 << 30  # rows per PCIe batch: ~1 GiB of X
+
+
+def _iter_nodes(chunks, engine: _PassEngine):
+    """Yield (node, n_input_chunks) for the stream.  Device chunks reduce in
+    place; host chunks are batched and double-buffered over a copy stream."""
+    t = dv.torch()
+    dev = dv.require_device()
+    pending_host = []
+
+    def flush_host(items):
+        yield from _reduce_host(items, engine, dev)
+
+    for ch in chunks:
+        if _is_device(ch.data):
+            if pending_host:
+                yield from flush_host(pending_host)
+                pending_host = []
+            x = dv.as_device_matrix(ch.data)
+            if x.shape[0] < 1:
+                raise UsageError(f"chunk must have at least one row, got shape {tuple(x.shape)}")
+            yield engine.reduce(x, int(ch.row_offset)), 1
+        else:
+            pending_host.append(ch)
+            if len(pending_host) >= 4096:
+                yield from flush_host(pending_host)
+                pending_host = []
+    if pending_host:
+        yield from flush_host(pending_host)
+    del t
+
+
+def _reduce_host(chunks, engine: _PassEngine, dev):
+    t = dv.torch()
+    copy_stream = t.cuda.Stream(dev)
+    compute_stream = t.cuda.current_stream(dev)
+    bufs: list = [None, None]
+    done_ev: list = [None, None]
+    ready_ev: list = [None, None]
+    hold: list = [None, None]  # host sources of in-flight copies
+    slot = 0
+    batch_rows = lambda n: max(1, HOST_BATCH_BYTES // (8 * n))  # noqa: E731
+    for pieces, consumed in _host_batches(chunks, batch_rows):
+        rows = sum(p[1].shape[0] for p in pieces)
+        n = pieces[0][1].shape[1]
+        buf = bufs[slot]
+        if buf is None or buf.shape[1] != n or buf.shape[0] < rows:
+            buf = t.empty((max(rows, batch_rows(n)), n), dtype=t.float64, device=dev)
+            bufs[slot] = buf
+        if ready_ev[slot] is not None:
+            ready_ev[slot].synchronize()  # copies two batches ago done: release their sources
+        hold[slot] = []
+        with t.cuda.stream(copy_stream):
+            if done_ev[slot] is not None:
+                copy_stream.wait_event(done_ev[slot])
+            pos = 0
+            for _, arr in pieces:
+                src = t.from_numpy(np.ascontiguousarray(arr))
+                hold[slot].append(src)
+                buf[pos:pos + arr.shape[0]].copy_(src, non_blocking=True)
+                pos += arr.shape[0]
+            ready = t.cuda.Event()
+            ready.record(copy_stream)
+        ready_ev[slot] = ready
+        compute_stream.wait_event(ready)
+        node = engine.reduce(buf[:rows], pieces[0][0])
+        ev = t.cuda.Event()
+        ev.record(compute_stream)
+        done_ev[slot] = ev
+        yield node, consumed
+        slot ^= 1
+
+
+def _run_pass(chunks, engine: _PassEngine, combine_order: str):
+    if combine_order not in COMBINE_ORDERS:
+        raise UsageError(f"combine_order must be one of {COMBINE_ORDERS}")
+    n_chunks = 0
+    depth = 0
+    if combine_order == "tree":
+        red = TreeReducer(_merge_nodes)
+        for node, consumed in _iter_nodes(chunks, engine):
+            n_chunks += consumed
+            red.push(node)
+        node = red.result()
+        depth = n_chunks.bit_length()  # TreeReducer depth over the input chunks (tsqr.py:232-234)
+    else:
+        node = None
+        for nd, consumed in _iter_nodes(chunks, engine):
+            n_chunks += consumed
+            node = nd if node is None else _merge_nodes(node, nd)
+    if node is None:
+        raise DataError("empty chunk stream")
+    return node, n_chunks, depth
+
+
+def stream_pass(chunks: Iterable[RowChunk], *, sketch_rows: int | None = None, seed: int = 0,
+                combine_order: str = "tree", threads: int = 1) -> StreamResult:
+    """One traversal of a chunk stream: the triangular factor, the column
+    norms and (with ``sketch_rows``) the Gaussian projection (reference
+    tsqr.py:276-343)."""
+    from .projection import SketchResult
+
+    if combine_order not in COMBINE_ORDERS:
+        raise UsageError(f"combine_order must be one of {COMBINE_ORDERS}")
+    if threads < 1:
+        raise UsageError(f"threads must be >= 1, got {threads}")
+    if sketch_rows is not None and sketch_rows < 1:
+        raise UsageError(f"sketch rows must be >= 1, got {sketch_rows}")
+    node, n_chunks, depth = _run_pass(chunks, _PassEngine(True, sketch_rows, seed, False), combine_order)
+    if node.rows < node.n:
+        raise DataError(f"not tall-and-skinny: m = {node.rows} < n = {node.n}")
+    stats = ColumnStats(l1=node.l1.cpu().numpy(), l2=np.sqrt(node.sq.cpu().numpy()))
+    sk = SketchResult(entries=node.sk.cpu().numpy(), seed=seed) if node.sk is not None else None
+    return StreamResult(factor=TriangularFactor(entries=node.r.cpu().numpy()), stats=stats, sketch=sk,
+                        rows=node.rows, chunks=n_chunks, tree_depth=depth)
+
+
+def gram_pass(chunks: Iterable[RowChunk], *, combine_order: str = "tree") -> GramResult:
+    """NEW: one pass producing X^T X and the column norms (the BASELINE
+    north-star Gram variant; no reference function)."""
+    node, n_chunks, depth = _run_pass(chunks, _PassEngine(False, None, 0, True), combine_order)
+    stats = ColumnStats(l1=node.l1.cpu().numpy(), l2=np.sqrt(node.sq.cpu().numpy()))
+    return GramResult(gram=node.g.cpu().numpy(), stats=stats, rows=node.rows, chunks=n_chunks, tree_depth=depth)
+
+
+__all__ = [
+    "COMBINE_ORDERS", "ColumnStats", "GramResult", "ReducedSVD", "StreamResult", "TreeReducer",
+    "TriangularFactor", "apply_column_scaling", "combine", "factor_chunk", "gram_pass", "rsvd", "stream_pass",
+]

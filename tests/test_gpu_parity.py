@@ -1,0 +1,273 @@
+"""Parity of the CUDA path with the reference (golden vectors) and the oracle on
+the same seeded inputs.  Tolerances: R normwise relative (rows sign-fixed on
+both sides, so no sign ambiguity) 1e-10 per the north star (observed ~1e-15);
+stats / sketch / Gram relative 1e-12; uniforms bit-exact; normals rtol 1e-12
+(the reference's own compiled-vs-python contract, test_kernels.py:40-49)."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1402_6964_b200 as tb
+from conftest import SMALL_CASES, rel_err
+from paper_1402_6964_b200 import device as dv
+from paper_1402_6964_b200 import streams
+
+pytestmark = pytest.mark.gpu
+R_TOL = 1e-10
+
+
+def dev(a):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device="cuda")
+
+
+# ---------------------------------------------------------------------------
+# RNG
+
+
+def test_rng_blocks_match_reference(golden_rng):
+    assert streams.get_backend() == "cuda-sm100a"
+    for (seed, tag), want in zip(golden_rng["seeds_tags"], golden_rng["streams"]):
+        assert streams.derive_stream(int(seed), int(tag)) == int(want)
+    for i, (s, start, cnt) in enumerate(golden_rng["blocks"]):
+        s, start, cnt = int(s), int(start), int(cnt)
+        assert np.array_equal(streams.uniform_block(s, start, cnt), golden_rng[f"uniform_{i}"])
+        np.testing.assert_allclose(streams.normal_block(s, start % 2**63, cnt), golden_rng[f"normal_{i}"],
+                                   rtol=1e-12, atol=1e-13)
+    np.testing.assert_allclose(streams.gaussian_rows(5, 0, 10, 4), golden_rng["gaussian_rows_5_0_10_4"],
+                               rtol=1e-12, atol=1e-13)
+    np.testing.assert_allclose(streams.gaussian_rows(3, 1000, 16, 9), golden_rng["gaussian_rows_3_1000_16_9"],
+                               rtol=1e-12, atol=1e-13)
+
+
+def test_rng_split_invariance_and_moments(oracle):
+    whole = streams.normal_block(9, 0, 500)
+    parts = np.concatenate([streams.normal_block(9, 0, 123), streams.normal_block(9, 123, 200),
+                            streams.normal_block(9, 323, 177)])
+    assert np.array_equal(whole, parts)
+    z = streams.normals(7, 0, 0, 10**6)
+    assert abs(z.mean()) < 0.01 and abs(z.var() - 1.0) < 0.02
+    u = streams.uniforms(7, 1, 0, 10**6)
+    assert u.min() >= 0.0 and u.max() < 1.0
+    np.testing.assert_allclose(z[:4096], oracle.normals(7, 0, 0, 4096), rtol=1e-12, atol=1e-13)
+
+
+# ---------------------------------------------------------------------------
+# TSQR factor / combine / stream_pass
+
+
+def test_spec_known_answers(golden_tsqr):
+    f = tb.factor_chunk(np.array([[3.0, 0], [4, 0], [0, 5]]))
+    np.testing.assert_allclose(f.entries, np.diag([5.0, 5.0]), atol=1e-15)
+    assert np.array_equal(tb.factor_chunk(np.array([[1.0, 2, 2]])).entries, golden_tsqr["fc_row"])
+    assert np.array_equal(tb.factor_chunk(np.array([[-1.0, 2, -2]])).entries, golden_tsqr["fc_negrow"])
+    np.testing.assert_allclose(tb.factor_chunk(golden_tsqr["fc_wide_in"]).entries, golden_tsqr["fc_wide"],
+                               atol=1e-14)
+    c = tb.combine(tb.TriangularFactor(np.diag([3.0, 4.0])), tb.TriangularFactor(np.diag([4.0, 3.0])))
+    np.testing.assert_allclose(c.entries, golden_tsqr["comb_diag"], atol=1e-15)
+    tri = np.triu(np.random.default_rng(1).uniform(0.5, 1, (5, 5)))
+    np.testing.assert_allclose(tb.factor_chunk(tri).entries, tri, rtol=1e-14, atol=1e-15)
+
+
+@pytest.mark.parametrize("name", SMALL_CASES)
+@pytest.mark.parametrize("size", [1, 7, 64, None])
+@pytest.mark.parametrize("where", ["device", "host"])
+def test_stream_pass_matches_reference(golden_tsqr, name, size, where):
+    x = golden_tsqr[f"{name}__x"]
+    size = x.shape[0] if size is None else size
+    key = f"{name}__c{size}__tree"
+    mk = dev if where == "device" else (lambda a: a)
+    chunks = [tb.RowChunk(o, mk(x[o:o + size])) for o in range(0, x.shape[0], size)]
+    res = tb.stream_pass(chunks, sketch_rows=6, seed=11)
+    assert rel_err(res.factor.entries, golden_tsqr[key + "__r"]) <= R_TOL
+    np.testing.assert_allclose(res.stats.l1, golden_tsqr[key + "__l1"], rtol=1e-12)
+    np.testing.assert_allclose(res.stats.l2, golden_tsqr[key + "__l2"], rtol=1e-12)
+    assert rel_err(res.sketch.entries, golden_tsqr[key + "__sketch"]) <= 1e-12
+    assert [res.rows, res.chunks, res.tree_depth] == list(golden_tsqr[key + "__meta"])
+    # RᵀR = XᵀX (reference SPEC.md:164)
+    rtr = res.factor.entries.T @ res.factor.entries
+    assert rel_err(rtr, x.T @ x) <= 1e-12
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 9, 15, 16, 17, 25, 31, 33, 64, 100, 127, 200, 255, 256, 300, 512])
+def test_factor_matches_oracle_many_widths(oracle, n):
+    rng = np.random.default_rng(n)
+    m = max(3 * n, 50) + 13
+    x = rng.standard_normal((m, n)) * np.logspace(0, -2, n)
+    f = tb.factor_chunk(dev(x))
+    want = oracle.factor_chunk(x)
+    assert rel_err(f.entries, want) <= R_TOL
+    assert np.array_equal(np.tril(f.entries, -1), np.zeros((n, n)))
+    assert (np.diagonal(f.entries) >= 0).all()
+
+
+@pytest.mark.parametrize("m", [2, 3, 10, 199, 200, 201, 1000, 12345, 100_003])
+def test_tall_shapes_and_tree_edges(oracle, m):
+    """Leaf counts that exercise non-power-of-two trees and partial blocks."""
+    rng = np.random.default_rng(m)
+    n = 40
+    x = rng.uniform(-1, 1, (m, n))
+    f = tb.factor_chunk(dev(x))
+    want = oracle.factor_chunk(x)
+    if m >= n:
+        assert rel_err(f.entries, want) <= R_TOL
+    else:  # rank deficient: rows beyond m are round-off debris on both sides
+        assert rel_err(f.entries.T @ f.entries, x.T @ x) <= 1e-12
+
+
+def test_combine_many_factors_tree_order(oracle):
+    rng = np.random.default_rng(5)
+    rs = [oracle.factor_chunk(rng.standard_normal((60, 20))) for _ in range(13)]
+    got = dv.combine_factors(dev(np.stack(rs))).cpu().numpy()
+    red = oracle.TreeReducer(oracle.combine)
+    for r in rs:
+        red.push(r)
+    assert rel_err(got, red.result()) <= R_TOL
+    z = tb.combine(tb.TriangularFactor(np.zeros((20, 20))), tb.TriangularFactor(rs[0]))
+    assert np.array_equal(z.entries, rs[0])
+
+
+def test_zero_and_duplicate_columns():
+    rng = np.random.default_rng(2)
+    x = rng.uniform(0, 1, (500, 12))
+    x[:, 3] = 0.0
+    x[:, 7] = x[:, 2]
+    res = tb.stream_pass([tb.RowChunk(0, dev(x))])
+    assert res.stats.l1[3] == 0.0 and res.stats.l2[3] == 0.0
+    r = res.factor.entries
+    assert rel_err(r.T @ r, x.T @ x) <= 1e-12
+    np.testing.assert_allclose(np.linalg.norm(r, axis=0), np.linalg.norm(x, axis=0), rtol=1e-12, atol=1e-14)
+
+
+def test_errors_match_reference():
+    with pytest.raises(tb.DataError, match="empty chunk stream"):
+        tb.stream_pass([])
+    with pytest.raises(tb.DataError, match="not tall-and-skinny"):
+        tb.stream_pass([tb.RowChunk(0, dev(np.ones((3, 5))))])
+    with pytest.raises(tb.UsageError):
+        tb.stream_pass([tb.RowChunk(0, dev(np.ones((9, 2))))], combine_order="bogus")
+    with pytest.raises(tb.UsageError):
+        tb.stream_pass([tb.RowChunk(0, dev(np.ones((9, 2))))], threads=0)
+    with pytest.raises(tb.UsageError):
+        tb.sketch_chunk(tb.RowChunk(0, dev(np.ones((9, 2)))), 0, 1)
+    with pytest.raises(tb.UsageError):
+        tb.factor_chunk(np.ones((0, 3)))
+    with pytest.raises(tb.UsageError):
+        tb.factor_chunk(np.ones((10, 4000)))  # beyond the on-chip block
+
+
+def test_sequential_and_first_come_orders(golden_tsqr):
+    x = golden_tsqr["tall_300x17__x"]
+    chunks = [tb.RowChunk(o, dev(x[o:o + 7])) for o in range(0, 300, 7)]
+    for order in ("sequential", "first-come"):
+        res = tb.stream_pass(chunks, combine_order=order, threads=4)
+        assert rel_err(res.factor.entries, golden_tsqr["tall_300x17__c7__sequential__r"]) <= R_TOL
+        assert res.tree_depth == 0
+
+
+def test_tree_result_deterministic():
+    x = np.random.default_rng(4).uniform(0, 1, (50_000, 64))
+    a = tb.factor_chunk(dev(x)).entries
+    b = tb.factor_chunk(dev(x)).entries
+    assert np.array_equal(a, b)
+
+
+# ---------------------------------------------------------------------------
+# sketch / Gram / stats
+
+
+def test_sketch_chunk_and_hook(oracle):
+    rng = np.random.default_rng(8)
+    x = rng.uniform(0, 1, (777, 30))
+    s = tb.sketch_chunk(tb.RowChunk(1000, dev(x)), 70, 3)
+    assert rel_err(s.entries, oracle.sketch_block(x, 1000, 70, 3)) <= 1e-12
+    g1 = np.zeros((777, 5))
+    g1[:, 0] = 1.0
+    hook = tb.sketch_chunk(tb.RowChunk(0, dev(x)), 5, 0, gaussian_rows_fn=lambda s_, o, r, k: g1)
+    np.testing.assert_allclose(hook.entries[0], x.sum(0), rtol=1e-13)
+    assert not hook.entries[1:].any()
+    # chunking invariance and linearity (SPEC sketch invariants)
+    halves = [tb.sketch_chunk(tb.RowChunk(o, dev(x[o:o + 400])), 70, 3) for o in (0, 400)]
+    whole = tb.sketch_chunk(tb.RowChunk(0, dev(x)), 70, 3)
+    assert rel_err(tb.merge_sketches(*halves).entries, whole.entries) <= 1e-13
+    twice = tb.sketch_chunk(tb.RowChunk(0, dev(2.0 * x)), 70, 3)
+    assert np.array_equal(twice.entries, 2.0 * whole.entries)
+
+
+@pytest.mark.parametrize("n", [1, 7, 16, 25, 64, 200, 256, 333, 512])
+def test_gram_matches_numpy(n):
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal((5000 + n, n))
+    g = tb.gram_pass([tb.RowChunk(0, dev(x))])
+    assert rel_err(g.gram, x.T @ x) <= 1e-13
+    assert np.array_equal(g.gram, g.gram.T)
+    np.testing.assert_allclose(g.stats.l1, np.abs(x).sum(0), rtol=1e-12)
+    np.testing.assert_allclose(g.stats.l2, np.linalg.norm(x, axis=0), rtol=1e-12)
+
+
+def test_gram_equivalence_invariant():
+    """‖RᵀR − XᵀX‖_F ≤ 1e-10 ‖XᵀX‖_F (reference SPEC.md:164) on the device outputs."""
+    x = np.random.default_rng(11).uniform(0, 1, (100_000, 50))
+    r = tb.factor_chunk(dev(x)).entries
+    g = tb.gram_pass([tb.RowChunk(0, dev(x))]).gram
+    assert rel_err(r.T @ r, g) <= 1e-10
+
+
+def test_column_stats_kernel():
+    x = np.random.default_rng(12).standard_normal((20_000, 33))
+    l1, sq = dv.column_stats(dev(x))
+    np.testing.assert_allclose(l1.cpu().numpy(), np.abs(x).sum(0), rtol=1e-12)
+    np.testing.assert_allclose(sq.cpu().numpy(), (x * x).sum(0), rtol=1e-12)
+
+
+# ---------------------------------------------------------------------------
+# BASELINE config C1 end to end (SURVEY §7 minimum slice)
+
+
+def test_c1_end_to_end_matches_reference(golden_c1, oracle):
+    spec = oracle.config_spec("C1")
+    x = oracle.config_rows(spec, 0, spec.m)
+    chunks = [tb.RowChunk(o, dev(x[o:o + 8192])) for o in range(0, spec.m, 8192)]
+    res = tb.stream_pass(chunks, sketch_rows=120, seed=0)
+    assert rel_err(res.factor.entries, golden_c1["r"]) <= R_TOL
+    assert rel_err(res.sketch.entries, golden_c1["sketch"]) <= 1e-12
+    np.testing.assert_allclose(res.stats.l1, golden_c1["l1"], rtol=1e-12)
+    red = tb.rsvd(res.factor)
+    k = tb.spa(red, 20, normalize=True, stats=res.stats)
+    assert list(k.indices) == list(golden_c1["k_spa"])
+    h = tb.compute_h(red, k)
+    assert np.abs(h.entries - golden_c1["h_spa"]).max() <= 1e-8
+    assert list(tb.xray_greedy(red, 20).indices) == list(golden_c1["k_xray"])
+    assert list(tb.gp_select(tb.scale_columns(res.sketch, res.stats), 20).indices) == list(golden_c1["k_gp"])
+
+
+@pytest.mark.parametrize("name", ["C1", "C4", "C5"])
+def test_device_generator_matches_oracle(oracle, name):
+    from paper_1402_6964_b200 import synthetic
+
+    spec = synthetic.config(name, m=20_000)
+    ospec = oracle.config_spec(name, m=20_000)
+    mix, planted, _ = synthetic.mixing(spec)
+    omix, oplanted, _ = oracle.config_mixing(ospec)
+    assert np.array_equal(mix, omix) and planted == oplanted
+    xd = synthetic.generate(spec, row0=5000, rows=3000).cpu().numpy()
+    xo = oracle.config_rows(ospec, 5000, 3000, omix)
+    assert rel_err(xd, xo) <= 1e-14
+    assert (xd >= 0).all()
+
+
+def test_sharded_world1_nccl(tmp_path):
+    import torch.distributed as dist
+
+    from paper_1402_6964_b200 import sharded
+
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", init_method=f"file://{tmp_path}/pg", rank=0, world_size=1)
+    try:
+        x = np.random.default_rng(6).uniform(0, 1, (4000, 24))
+        res, g = sharded.sharded_stream_pass(dev(x), 0, sketch_rows=8, seed=2, with_gram=True)
+        ref = tb.stream_pass([tb.RowChunk(0, dev(x))], sketch_rows=8, seed=2)
+        assert rel_err(res.factor.entries, ref.factor.entries) <= 1e-14
+        assert rel_err(g, x.T @ x) <= 1e-13
+    finally:
+        dist.destroy_process_group()

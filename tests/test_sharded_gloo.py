@@ -1,0 +1,76 @@
+"""Multi-rank exchange of the row-sharded pass (paper_1402_6964_b200.sharded)
+on CPU with gloo, world_size 2: each rank reduces its shard (oracle as the
+per-rank reducer — test infrastructure), the product's exchange() all-gathers
+the packed partials and combines them in TreeReducer order; the replicated
+result must equal the single-process oracle pass and be identical on both
+ranks."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import ROOT
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _oracle_combine_stack(rs):
+    from oracle import tsnmf_oracle as o
+
+    red = o.TreeReducer(o.combine)
+    for r in rs.numpy():
+        red.push(r)
+    return torch.from_numpy(red.result())
+
+
+def _worker(rank, world, port, x, k, seed, out_dir):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import tsnmf_oracle as o
+        from paper_1402_6964_b200 import sharded
+
+        lo, hi = sharded.shard_range(x.shape[0], world, rank)
+        xs = x[lo:hi]
+        r = o.factor_chunk(xs)
+        l1, sq = o.block_stats(xs)
+        sk = o.sketch_block(xs, lo, k, seed)
+        g = xs.T @ xs
+        part = sharded.ShardPartials(r=torch.from_numpy(r), l1=torch.from_numpy(l1), sumsq=torch.from_numpy(sq),
+                                     rows=hi - lo, sketch=torch.from_numpy(sk), gram=torch.from_numpy(g))
+        out = sharded.exchange(part, _oracle_combine_stack)
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), r=out.r.numpy(), l1=out.l1.numpy(),
+                 sq=out.sumsq.numpy(), sk=out.sketch.numpy(), g=out.gram.numpy(), rows=out.rows)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_exchange_matches_single_pass(tmp_path, world, oracle):
+    rng = np.random.default_rng(3)
+    x = rng.uniform(0, 1, (901, 13))
+    k, seed = 5, 9
+    mp.spawn(_worker, args=(world, _free_port(), x, k, seed, str(tmp_path)), nprocs=world, join=True)
+    outs = [np.load(tmp_path / f"rank{r}.npz") for r in range(world)]
+    for key in ("r", "l1", "sq", "sk", "g"):
+        assert np.array_equal(outs[0][key], outs[1][key]), f"ranks disagree on {key}"
+    ref = oracle.stream_pass(oracle.chunks_of(x, 451), sketch_rows=k, seed=seed)
+    r = outs[0]
+    assert np.linalg.norm(r["r"] - ref.r) / np.linalg.norm(ref.r) < 1e-13
+    np.testing.assert_allclose(r["l1"], ref.l1, rtol=1e-13)
+    np.testing.assert_allclose(r["sq"], ref.sumsq, rtol=1e-13)
+    np.testing.assert_allclose(r["sk"], ref.sketch, rtol=1e-11, atol=1e-12)
+    np.testing.assert_allclose(r["g"], x.T @ x, rtol=1e-12)
+    assert int(r["rows"]) == x.shape[0]
