@@ -13,7 +13,7 @@ import os
 from .errors import DataError, NumericalError, TsnmfError, UsageError
 
 LIB_NAME = "libtsnmf_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+LIB_PATH = os.environ.get("TSNMF_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 ABI_VERSION = 1
 
 OP_TSQR, OP_COMBINE, OP_GRAM, OP_SKETCH, OP_STATS = 1, 2, 3, 4, 5

@@ -18,7 +18,7 @@ constexpr int kGrThreads = 256;
 constexpr int kGrWarps = kGrThreads / 32;
 constexpr int kGrSpw = 6;                       // super-tiles per warp
 constexpr int kGrSpc = kGrWarps * kGrSpw;       // super-tiles per CTA (tile group)
-constexpr int kGrBr = 32;                       // rows per stage
+constexpr int kGrBrMax = 32;                    // rows per stage (16 when a 32-row double buffer does not fit)
 
 struct GrGeom {
   int n, npad;  // npad = round_up(n, 16)
@@ -26,6 +26,7 @@ struct GrGeom {
   int ns;       // super-blocks per side (npad / 16)
   int nst;      // super-tiles in the upper triangle
   int groups;   // tile groups
+  int br;       // rows per stage
   int64_t rows_per_split;
 };
 
@@ -50,7 +51,8 @@ __global__ void __launch_bounds__(kGrThreads, 2)
   const int64_t rbeg = split * g.rows_per_split;
   const int64_t rend = min64(m, rbeg + g.rows_per_split);
   const int lds = g.lds;
-  double* buf[2] = {smem, smem + kGrBr * lds};
+  double* buf[2] = {smem, smem + g.br * lds};
+  const int br = g.br;
   const bool vec16 = ((ldx & 1) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
 
   int stP[kGrSpw], stQ[kGrSpw];
@@ -72,15 +74,15 @@ __global__ void __launch_bounds__(kGrThreads, 2)
   double l1a[2] = {0.0, 0.0};
   const bool do_l1 = (group == 0) && (l1part != nullptr);
 
-  const int64_t nstages = ceil_div(max64(rend - rbeg, 0), kGrBr);
+  const int64_t nstages = ceil_div(max64(rend - rbeg, 0), g.br);
   if (nstages > 0) {
-    stage_rows(buf[0], lds, x + rbeg * ldx, ldx, (int)min64(kGrBr, rend - rbeg), g.n, kGrBr, g.npad, vec16);
+    stage_rows(buf[0], lds, x + rbeg * ldx, ldx, (int)min64(g.br, rend - rbeg), g.n, g.br, g.npad, vec16);
     cp_async_commit();
   }
   for (int64_t s = 0; s < nstages; ++s) {
     if (s + 1 < nstages) {
-      const int64_t r0 = rbeg + (s + 1) * kGrBr;
-      stage_rows(buf[(s + 1) & 1], lds, x + r0 * ldx, ldx, (int)min64(kGrBr, rend - r0), g.n, kGrBr,
+      const int64_t r0 = rbeg + (s + 1) * g.br;
+      stage_rows(buf[(s + 1) & 1], lds, x + r0 * ldx, ldx, (int)min64(g.br, rend - r0), g.n, g.br,
                  g.npad, vec16);
       cp_async_commit();
       cp_async_wait<1>();
@@ -96,13 +98,13 @@ __global__ void __launch_bounds__(kGrThreads, 2)
         if (col < g.n) {
           double a = l1a[h];
 #pragma unroll 8
-          for (int i = 0; i < kGrBr; ++i) a += fabs(xs[i * lds + col]);
+          for (int i = 0; i < br; ++i) a += fabs(xs[i * lds + col]);
           l1a[h] = a;
         }
       }
     }
 #pragma unroll 2
-    for (int i = 0; i < kGrBr; i += 4) {
+    for (int i = 0; i < br; i += 4) {
       const double* row = xs + (i + (lane & 3)) * lds + (lane >> 2);
 #pragma unroll
       for (int u = 0; u < kGrSpw; ++u) {
@@ -177,13 +179,14 @@ GrGeom gr_geom(int64_t m, int n, int sms) {
   g.ns = g.npad / 16;
   g.nst = g.ns * (g.ns + 1) / 2;
   g.groups = (int)ceil_div(g.nst, kGrSpc);
+  g.br = (2 * kGrBrMax * g.lds * 8 <= 227 * 1024) ? kGrBrMax : kGrBrMax / 2;
   const int64_t target = max64(1, (int64_t)2 * sms / g.groups);
-  const int64_t splits = max64(1, min64(target, ceil_div(m, 4 * kGrBr)));
-  g.rows_per_split = round_up(ceil_div(m, splits), kGrBr);
+  const int64_t splits = max64(1, min64(target, ceil_div(m, 4 * g.br)));
+  g.rows_per_split = round_up(ceil_div(m, splits), g.br);
   return g;
 }
 
-size_t gr_smem(const GrGeom& g) { return sizeof(double) * 2 * kGrBr * (size_t)g.lds; }
+size_t gr_smem(const GrGeom& g) { return sizeof(double) * 2 * g.br * (size_t)g.lds; }
 
 int64_t gr_splits(int64_t m, const GrGeom& g) { return max64(1, ceil_div(m, g.rows_per_split)); }
 

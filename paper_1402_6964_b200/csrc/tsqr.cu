@@ -22,51 +22,398 @@ namespace tsnmf {
 
 constexpr int kTqThreads = 256;
 constexpr int kTqWarps = kTqThreads / 32;
-constexpr int kMaxRpt = 8;  // panel rows per thread
+constexpr int kNB = 8;       // panel width (reflectors per compact-WY block)
+constexpr int kMaxRq = 4;    // block rows per lane of each panel warp (block rows <= 256)
 
 struct TqGeom {
   int n;      // data columns
-  int npad;   // padded columns (multiple of NB); R slots are npad x npad
-  int lds;    // shared-memory row stride of the block
-  int brows;  // rows per block (multiple of 8, <= (256/NB) * kMaxRpt)
+  int npad;   // padded columns (multiple of 8); R slots are npad x npad
+  int lds;    // shared-memory row stride of the block (% 16 == 8)
+  int brows;  // rows per block (multiple of 8, <= 64 * kMaxRq)
 };
 
-template <int NB>
 struct TqLayout {
-  static constexpr int kSlots = kTqThreads / NB;
   // offsets in doubles from the dynamic smem base
-  __host__ __device__ static int rd(const TqGeom& g) { return g.brows * g.lds; }
-  __host__ __device__ static int tm(const TqGeom& g) { return rd(g) + NB * NB; }
-  __host__ __device__ static int tcol(const TqGeom& g) { return tm(g) + NB * NB; }
-  __host__ __device__ static int tau(const TqGeom& g) { return tcol(g) + NB * NB; }
-  __host__ __device__ static int part(const TqGeom& g) { return tau(g) + NB; }
-  __host__ __device__ static int wsc(const TqGeom& g) { return part(g) + 2 * kTqWarps * NB; }
-  __host__ __device__ static int total(const TqGeom& g) { return wsc(g) + kTqWarps * NB * 8; }
+  __host__ __device__ static int rp(const TqGeom& g) { return g.brows * g.lds; }            // 2 x 8 R rows (stride lds)
+  __host__ __device__ static int tm(const TqGeom& g) { return rp(g) + 2 * kNB * g.lds; }    // 2 x 8x8 T
+  __host__ __device__ static int red(const TqGeom& g) { return tm(g) + 2 * kNB * kNB; }    // 2 x 32 x 9 partials
+  __host__ __device__ static int xch(const TqGeom& g) { return red(g) + 2 * 32 * 9; }       // 2 x 16 exchange
+  __host__ __device__ static int wsc(const TqGeom& g) { return xch(g) + 32; }                // per-warp 8x8 scratch
+  __host__ __device__ static int wpart(const TqGeom& g) { return wsc(g) + kTqWarps * kNB * 8; }  // 6 partial W + W'
+  __host__ __device__ static int total(const TqGeom& g) { return wpart(g) + 7 * 64; }
   static size_t bytes(const TqGeom& g) { return sizeof(double) * (size_t)total(g); }
 };
 
+// Shared-memory swizzle of the block: column c of row r lives at r*lds + (c ^ swz(r)).  With
+// lds % 16 == 8 this makes every DMMA fragment access conflict-free: the 4x8 operand slabs (lane:
+// row l%4, col l/4), the V fragments (row l/4, col l%4) and the 16-byte C-tile rows (row l/4,
+// col 2*(l%4)).  XOR by 0 or 4 permutes inside aligned 8-column groups, so 16-byte pairs stay intact.
+__device__ __forceinline__ int swz(int row) { return (row & 2) << 1; }
+
+// Named barriers between the panel warp (warp 0) and the GEMM warps (1..7).
+// Warp roles: warps 0 and 4 (both on SMSP 0) = panel warps, so SMSP 0 runs the panel's latency-bound
+// FP64 chain without DMMA traffic; warps 1,2,3,5,6,7 = GEMM warps (GEMM warp 0 also stages R rows).
+constexpr int kBarColsReady = 1;  // next panel's columns updated + its R rows staged  (GEMM, helper -> panel)
+constexpr int kBarPanelDone = 2;  // V, T of the current panel published               (panel -> GEMM, helper)
+constexpr int kBarGemm = 3;       // among the 6 GEMM warps (cooperative lookahead update)
+constexpr int kGemmWarps = 6;
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ int gemm_index(int warp) { return warp < 4 ? warp - 1 : warp - 2; }  // 0..5
+
+#ifdef TSNMF_TRACE
+// CTA 0, first row block only: g_trace[warp][panel * 64 + tag] = clock64() (fire-and-forget stores)
+__device__ long long g_trace[8][64 * 64];
+#define TQ_TRACE(tag)                                                                  \
+  do {                                                                                 \
+    if (tq_p >= 0 && blockIdx.x == 0 && (threadIdx.x & 31) == 0)                       \
+      g_trace[threadIdx.x >> 5][tq_p * 64 + (tag)] = clock64();                        \
+  } while (0)
+#else
+#define TQ_TRACE(tag) \
+  do {                \
+    (void)tq_p;       \
+  } while (0)
+#endif
+
+// Panel factorization of columns [j0, j0 + 8) by the TWO panel warps (warps 0 and 4, both on SMSP 0,
+// which carries no DMMA traffic).  Panel warp h holds block rows [h*half, (h+1)*half) in registers,
+// row = h*half + lane + 32 q.  Per column: dot products of the current column with all 8 panel
+// columns (its norm, the trailing dots for the update, the V^T v dots for T) are reduced within each
+// warp by a transposed shared-memory sum, the two warp totals are exchanged through shared memory with
+// one 64-thread named barrier and added in fixed order (both warps get bit-identical totals, so they
+// compute identical reflectors).  Reflector (dlarfg convention): beta = -sign(alpha) ||(alpha, x)||,
+// tau = (beta - alpha)/beta, v = x/(alpha - beta).  T (upper triangular, dlarft forward columnwise) is
+// built incrementally off the critical path; R row entries are kept in registers (lane c owns column
+// c) and stored once per panel.  Rd: the 8 R rows of this panel staged in shared memory (stride ldr).
+constexpr int kBarPanelPair = 4;
+
+template <int RQ, int NPW>
+__device__ __forceinline__ void panel_factor(double* __restrict__ Bs, int lds, int brows, int j0,
+                                             double* __restrict__ R, int npad, const double* __restrict__ Rd,
+                                             int ldr, double* __restrict__ Tm, double* __restrict__ red,
+                                             double* __restrict__ xch, int h, int lane, int tq_p) {
+  const int half = NPW == 2 ? (brows + 1) / 2 : brows;
+  const int row0 = h * half;
+  const int rows_mine = h == 0 ? half : brows - half;
+  const int sw = swz(row0 + lane);  // half is a multiple of 4 -> (row & 2) = (lane & 2)
+  double x[RQ][kNB];
+#pragma unroll
+  for (int q = 0; q < RQ; ++q) {
+    const int rl = lane + 32 * q;
+#pragma unroll
+    for (int c = 0; c < kNB; ++c) x[q][c] = (rl < rows_mine) ? Bs[(row0 + rl) * lds + j0 + (c ^ sw)] : 0.0;
+  }
+  double trow[kNB], rmine[kNB];
+#pragma unroll
+  for (int c = 0; c < kNB; ++c) trow[c] = rmine[c] = 0.0;
+  double* redw = red + h * (32 * 9);
+  const int rc = lane & 7, rq = lane >> 3;  // reduction role: column, quarter of the warp
+#pragma unroll
+  for (int jj = 0; jj < kNB; ++jj) {
+    TQ_TRACE(10 + jj);
+#pragma unroll
+    for (int c = 0; c < kNB; ++c) {
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < RQ; ++q) acc = fma(x[q][jj], x[q][c], acc);
+      redw[lane * 9 + c] = acc;
+    }
+    __syncwarp();
+    const double s0 = redw[(rq * 8 + 0) * 9 + rc] + redw[(rq * 8 + 1) * 9 + rc];
+    const double s1 = redw[(rq * 8 + 2) * 9 + rc] + redw[(rq * 8 + 3) * 9 + rc];
+    const double s2 = redw[(rq * 8 + 4) * 9 + rc] + redw[(rq * 8 + 5) * 9 + rc];
+    const double s3 = redw[(rq * 8 + 6) * 9 + rc] + redw[(rq * 8 + 7) * 9 + rc];
+    double tot = (s0 + s1) + (s2 + s3);
+    tot += __shfl_xor_sync(0xffffffffu, tot, 8);
+    tot += __shfl_xor_sync(0xffffffffu, tot, 16);
+    double d[kNB];
+    if (NPW == 2) {
+      double* xw = xch + (jj & 1) * 16;  // double-buffered exchange slots
+      if (lane < 8) xw[h * 8 + lane] = tot;
+      named_sync(kBarPanelPair, 64);
+#pragma unroll
+      for (int c = 0; c < kNB; ++c) d[c] = xw[c] + xw[8 + c];
+    } else {
+#pragma unroll
+      for (int c = 0; c < kNB; ++c) d[c] = __shfl_sync(0xffffffffu, tot, c);
+    }
+    TQ_TRACE(30 + jj);
+    const double alpha = Rd[jj * ldr + j0 + jj];
+    double tau = 0.0, scale = 0.0, beta = alpha;
+    if (d[jj] > 0.0) {
+      // inv = 1/||(alpha, x)||;  tau = (beta - alpha)/beta = 1 + |alpha| inv;  scale = sign(alpha)/(|alpha| + nrm)
+      const double ss = fma(alpha, alpha, d[jj]);
+      const double inv = rsqrt(ss);
+      const double nrm = ss * inv;
+      beta = -copysign(nrm, alpha);
+      tau = fma(fabs(alpha), inv, 1.0);
+      scale = copysign(__drcp_rn(fabs(alpha) + nrm), alpha);
+    }
+#pragma unroll
+    for (int c = jj + 1; c < kNB; ++c) {
+      const double rjc = Rd[jj * ldr + j0 + c];
+      const double tw = tau * fma(scale, d[c], rjc);
+      const double f = tw * scale;
+#pragma unroll
+      for (int q = 0; q < RQ; ++q) x[q][c] = fma(-f, x[q][jj], x[q][c]);
+      if (lane == c) rmine[jj] = rjc - tw;
+    }
+#pragma unroll
+    for (int q = 0; q < RQ; ++q) x[q][jj] *= scale;
+    if (lane == jj) rmine[jj] = beta;
+    {  // T[r][jj] = -tau_jj * sum_{q=r}^{jj-1} T[r][q] (v_q^T v_jj),  v_q^T v_jj = scale * d[q]
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < jj; ++q) acc = fma(trow[q], d[q], acc);
+      trow[jj] = (lane == jj) ? tau : (lane < jj ? -tau * scale * acc : 0.0);
+    }
+    __syncwarp();  // redw reuse
+  }
+#pragma unroll
+  for (int q = 0; q < RQ; ++q) {
+    const int rl = lane + 32 * q;
+    if (rl < rows_mine) {
+#pragma unroll
+      for (int c = 0; c < kNB; ++c) Bs[(row0 + rl) * lds + j0 + (c ^ sw)] = x[q][c];
+    }
+  }
+  if (h == 0 && lane < kNB) {
+    double* Rcol = R + (int64_t)j0 * npad + j0 + lane;  // lane c writes R(j0 + jj, j0 + c), jj <= c
+#pragma unroll
+    for (int jj = 0; jj < kNB; ++jj)
+      if (jj <= lane) Rcol[(int64_t)jj * npad] = rmine[jj];
+#pragma unroll
+    for (int c = 0; c < kNB; ++c) Tm[lane * kNB + c] = trow[c];
+  }
+}
+
+// Stage rows into the swizzled block layout (cp.async); zero-fill padding rows / columns.
+__device__ __forceinline__ void stage_block(double* __restrict__ dst, int lds, const double* __restrict__ src,
+                                            int64_t ldsrc, int nrows, int ncols, int rows_total, int cols_total,
+                                            bool vec16) {
+  const int tid = threadIdx.x;
+  if (vec16) {
+    const int pairs = ncols >> 1;
+    for (int idx = tid; idx < nrows * pairs; idx += kTqThreads) {
+      const int r = idx / pairs, c = (idx - r * pairs) * 2;
+      cp_async16(dst + r * lds + (c ^ swz(r)), src + r * ldsrc + c);
+    }
+    if (ncols & 1)
+      for (int r = tid; r < nrows; r += kTqThreads)
+        cp_async8(dst + r * lds + ((ncols - 1) ^ swz(r)), src + r * ldsrc + ncols - 1);
+  } else {
+    for (int idx = tid; idx < nrows * ncols; idx += kTqThreads) {
+      const int r = idx / ncols, c = idx - r * ncols;
+      cp_async8(dst + r * lds + (c ^ swz(r)), src + r * ldsrc + c);
+    }
+  }
+  const int pad = cols_total - ncols;
+  if (pad > 0)
+    for (int idx = tid; idx < nrows * pad; idx += kTqThreads) {
+      const int r = idx / pad, c = ncols + (idx - r * pad);
+      dst[r * lds + (c ^ swz(r))] = 0.0;
+    }
+  for (int idx = tid; idx < (rows_total - nrows) * cols_total; idx += kTqThreads) {
+    const int r = nrows + idx / cols_total, c = idx % cols_total;
+    dst[r * lds + c] = 0.0;
+  }
+}
+
+// Stage the 8 R rows j0 .. j0+7 (columns [j0, npad)) into shared memory (stride ldr), by `nthr` threads
+// starting at thread index t0 (cp.async 16-byte copies; npad is a multiple of 8).
+__device__ __forceinline__ void stage_rrows(double* __restrict__ dst, int ldr, const double* __restrict__ R, int npad,
+                                            int j0, int t, int nthr) {
+  const int pairs = (npad - j0) >> 1;
+  for (int idx = t; idx < kNB * pairs; idx += nthr) {
+    const int r = idx / pairs, c = j0 + 2 * (idx - r * pairs);
+    cp_async16(dst + r * ldr + c, R + (int64_t)(j0 + r) * npad + c);
+  }
+}
+
+// Apply panel (j0)'s block reflector  Q^T = I - V T^T V^T  to column blocks cbs[0..G) of [R; B]:
+//   W = R_p(:, cb) + V^T B(:, cb);  W' = T^T W;  R_p(:, cb) -= W';  B(:, cb) -= V W'.
+// One warp, no CTA barrier.  R_p comes from the staged rows Rp (stride ldr); R is updated in global.
+template <int G>
+__device__ __forceinline__ void update_cbs(double* __restrict__ Bs, int lds, int brows, int j0,
+                                           const double* __restrict__ Rp, int ldr, double* __restrict__ R, int npad,
+                                           const double* __restrict__ Tm, double* __restrict__ Wsc, const int (&cbs)[G],
+                                           int lane, int tq_p) {
+  const int frag_col = (lane >> 2) ^ ((lane & 2) << 1);  // slab fragment: row i + l%4, col l/4
+  const int vsw = ((lane >> 2) & 2) << 1;                // V / C-tile rows 8rb + l/4
+  double acc0[G][2], acc1[G][2];
+#pragma unroll
+  for (int gg = 0; gg < G; ++gg) {
+    const double* rp = Rp + (lane >> 2) * ldr + 8 * cbs[gg] + 2 * (lane & 3);
+    acc0[gg][0] = rp[0];
+    acc0[gg][1] = rp[1];
+    acc1[gg][0] = acc1[gg][1] = 0.0;
+  }
+  TQ_TRACE(20);
+  // W = R_p + V^T B: K = brows in steps of 4 rows, two independent accumulator chains
+  const double* slab = Bs + (lane & 3) * lds + frag_col;
+#pragma unroll 2
+  for (int i = 0; i < brows; i += 8) {
+    const double* r0 = slab + i * lds;
+    const double* r1 = r0 + 4 * lds;
+    const double a0 = r0[j0], a1 = r1[j0];
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg) {
+      dmma(acc0[gg][0], acc0[gg][1], a0, r0[8 * cbs[gg]]);
+      dmma(acc1[gg][0], acc1[gg][1], a1, r1[8 * cbs[gg]]);
+    }
+  }
+  TQ_TRACE(21);
+  // W' = T^T W ; R_p -= W' ; gather -W' as B-operand fragments
+  double wb[G][2];
+#pragma unroll
+  for (int gg = 0; gg < G; ++gg) {
+    Wsc[(lane >> 2) * 8 + 2 * (lane & 3)] = acc0[gg][0] + acc1[gg][0];
+    Wsc[(lane >> 2) * 8 + 2 * (lane & 3) + 1] = acc0[gg][1] + acc1[gg][1];
+    __syncwarp();
+    double w0 = 0.0, w1 = 0.0;
+#pragma unroll
+    for (int k0 = 0; k0 < 8; k0 += 4)
+      dmma(w0, w1, Tm[(k0 + (lane & 3)) * kNB + (lane >> 2)], Wsc[(k0 + (lane & 3)) * 8 + (lane >> 2)]);
+    const double* rps = Rp + (lane >> 2) * ldr + 8 * cbs[gg] + 2 * (lane & 3);
+    double* rp = R + (int64_t)(j0 + (lane >> 2)) * npad + 8 * cbs[gg] + 2 * (lane & 3);
+    rp[0] = rps[0] - w0;
+    rp[1] = rps[1] - w1;
+    __syncwarp();
+    Wsc[(lane >> 2) * 8 + 2 * (lane & 3)] = w0;
+    Wsc[(lane >> 2) * 8 + 2 * (lane & 3) + 1] = w1;
+    __syncwarp();
+#pragma unroll
+    for (int k4 = 0; k4 < 2; ++k4) wb[gg][k4] = -Wsc[(4 * k4 + (lane & 3)) * 8 + (lane >> 2)];
+    __syncwarp();
+  }
+  TQ_TRACE(22);
+  // B -= V W'   (C tiles read/written in place; K = 8), two row blocks per iteration
+#pragma unroll 1
+  for (int rb = 0; rb < brows / 8; rb += 2) {
+    double* rowa = Bs + (8 * rb + (lane >> 2)) * lds;
+    double* rowb = rowa + 8 * lds;
+    const bool two = rb + 1 < brows / 8;
+    const double a0 = rowa[j0 + ((lane & 3) ^ vsw)], a1 = rowa[j0 + ((4 + (lane & 3)) ^ vsw)];
+    const double b0 = two ? rowb[j0 + ((lane & 3) ^ vsw)] : 0.0;
+    const double b1 = two ? rowb[j0 + ((4 + (lane & 3)) ^ vsw)] : 0.0;
+    double2 ca[G], cb2[G];
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg) {
+      ca[gg] = *reinterpret_cast<const double2*>(rowa + 8 * cbs[gg] + ((2 * (lane & 3)) ^ vsw));
+      if (two) cb2[gg] = *reinterpret_cast<const double2*>(rowb + 8 * cbs[gg] + ((2 * (lane & 3)) ^ vsw));
+    }
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg) {
+      dmma(ca[gg].x, ca[gg].y, a0, wb[gg][0]);
+      if (two) dmma(cb2[gg].x, cb2[gg].y, b0, wb[gg][0]);
+    }
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg) {
+      dmma(ca[gg].x, ca[gg].y, a1, wb[gg][1]);
+      if (two) dmma(cb2[gg].x, cb2[gg].y, b1, wb[gg][1]);
+    }
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg) {
+      *reinterpret_cast<double2*>(rowa + 8 * cbs[gg] + ((2 * (lane & 3)) ^ vsw)) = ca[gg];
+      if (two) *reinterpret_cast<double2*>(rowb + 8 * cbs[gg] + ((2 * (lane & 3)) ^ vsw)) = cb2[gg];
+    }
+  }
+  TQ_TRACE(23);
+}
+
+
+// Cooperative lookahead: the 6 GEMM warps apply panel (j0)'s reflector to the single column block cb
+// (the next panel's columns).  GEMM1 is split over rows (k-step i/4 = gi mod 6) into 6 partial W tiles
+// summed in fixed order by GEMM warp 0, which also forms W' = T^T W and updates R; then each warp
+// updates its row blocks (rb = gi mod 6).  Two barriers among the GEMM warps only.
+__device__ __forceinline__ void lookahead_cb(double* __restrict__ Bs, int lds, int brows, int j0,
+                                             const double* __restrict__ Rp, int ldr, double* __restrict__ R, int npad,
+                                             const double* __restrict__ Tm, double* __restrict__ Wpart, int cb,
+                                             int gi, int lane) {
+  const int frag_col = (lane >> 2) ^ ((lane & 2) << 1);
+  const int vsw = ((lane >> 2) & 2) << 1;
+  double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+  const double* slab = Bs + (lane & 3) * lds + frag_col;
+  int it = 0;
+  for (int i = 4 * gi; i < brows; i += 4 * kGemmWarps, ++it) {
+    const double* r = slab + i * lds;
+    if (it & 1) dmma(e0, e1, r[j0], r[8 * cb]);
+    else dmma(c0, c1, r[j0], r[8 * cb]);
+  }
+  const int ci = (lane >> 2) * 8 + 2 * (lane & 3);
+  Wpart[gi * 64 + ci] = c0 + e0;
+  Wpart[gi * 64 + ci + 1] = c1 + e1;
+  named_sync(kBarGemm, 32 * kGemmWarps);
+  double* Wsh = Wpart + 6 * 64;
+  if (gi == 0) {
+    const double* rps = Rp + (lane >> 2) * ldr + 8 * cb + 2 * (lane & 3);
+    double w0 = rps[0], w1 = rps[1];
+#pragma unroll
+    for (int g = 0; g < kGemmWarps; ++g) {
+      w0 += Wpart[g * 64 + ci];
+      w1 += Wpart[g * 64 + ci + 1];
+    }
+    __syncwarp();
+    Wsh[ci] = w0;  // W (natural row-major 8x8)
+    Wsh[ci + 1] = w1;
+    __syncwarp();
+    double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+    for (int k0 = 0; k0 < 8; k0 += 4)
+      dmma(v0, v1, Tm[(k0 + (lane & 3)) * kNB + (lane >> 2)], Wsh[(k0 + (lane & 3)) * 8 + (lane >> 2)]);
+    double* rp = R + (int64_t)(j0 + (lane >> 2)) * npad + 8 * cb + 2 * (lane & 3);
+    rp[0] = rps[0] - v0;
+    rp[1] = rps[1] - v1;
+    __syncwarp();
+    Wsh[ci] = v0;  // W'
+    Wsh[ci + 1] = v1;
+  }
+  named_sync(kBarGemm, 32 * kGemmWarps);
+  const double wb0 = -Wsh[(lane & 3) * 8 + (lane >> 2)];
+  const double wb1 = -Wsh[(4 + (lane & 3)) * 8 + (lane >> 2)];
+  for (int rb = gi; rb < brows / 8; rb += kGemmWarps) {
+    double* rowp = Bs + (8 * rb + (lane >> 2)) * lds;
+    const double a0 = rowp[j0 + ((lane & 3) ^ vsw)], a1 = rowp[j0 + ((4 + (lane & 3)) ^ vsw)];
+    double2* cp = reinterpret_cast<double2*>(rowp + 8 * cb + ((2 * (lane & 3)) ^ vsw));
+    double2 cv = *cp;
+    dmma(cv.x, cv.y, a0, wb0);
+    dmma(cv.x, cv.y, a1, wb1);
+    *cp = cv;
+  }
+}
+
 // Fold `nrows` data rows (row-major, stride ldsrc, `ncols` real columns) into the R slot `R`.
-// triangular: data row i is zero left of column i (data is another R factor).
-template <int NB>
+// triangular: data row i is zero left of column i (the data is another R factor).
+//
+// Lookahead schedule per panel p (warp 0 = panel warp on SMSP 0, warp 4 = helper, 6 GEMM warps):
+//   panel warp : wait ColsReady(p) -> factor panel p -> arrive PanelDone(p)
+//   helper     : wait PanelDone(p) -> stage R rows of panel p+1 -> arrive ColsReady(p+1)
+//   GEMM warps : wait PanelDone(p) -> cooperatively update column block p+1 -> arrive ColsReady(p+1)
+//                -> update column blocks p+2.. with panel p
+// so panel p+1 is factored while the trailing update of panel p runs.  V_p lives in the block's
+// panel-p columns (never touched again this block); T and the staged R rows are double-buffered.
+template <int RQ, int NPW>
 __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src, int64_t nrows, int64_t ldsrc,
                           int ncols, const TqGeom g, bool triangular, bool init_zero,
                           double* __restrict__ stats_out, double* smem) {
-  using L = TqLayout<NB>;
-  constexpr int kSlots = L::kSlots;
+  using L = TqLayout;
   constexpr int G = 4;  // column blocks per GEMM group
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int npad = g.npad, lds = g.lds, brows = g.brows;
   double* Bs = smem;
-  double* Rd = smem + L::rd(g);
+  double* Rp = smem + L::rp(g);
   double* Tm = smem + L::tm(g);
-  double* Tcol = smem + L::tcol(g);
-  double* tau_s = smem + L::tau(g);
-  double* part = smem + L::part(g);
-  double* Wsc = smem + L::wsc(g) + warp * NB * 8;
-
-  const int c = tid % NB, s = tid / NB;
-  const int rpt = (brows + kSlots - 1) / kSlots;
-  const int npanels = npad / NB, ncb = npad / 8;
+  double* red = smem + L::red(g);
+  double* Wsc = smem + L::wsc(g) + warp * kNB * 8;
+  double* Wpart = smem + L::wpart(g);
+  double* xch = smem + L::xch(g);
+  const int npanels = npad / kNB, ncb = npad / 8;
+  const int ldr = lds;
   const bool vec16 = ((ldsrc & 1) == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
 
   if (init_zero) {
@@ -76,8 +423,10 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
 
   for (int64_t r0 = 0; r0 < nrows; r0 += brows) {
     const int cnt = (int)min64(brows, nrows - r0);
-    __syncthreads();  // previous block fully consumed; R init visible
-    stage_rows(Bs, lds, src + r0 * ldsrc, ldsrc, cnt, ncols, brows, npad, vec16);
+    const int p0 = triangular ? (int)min64(r0 / kNB, npanels) : 0;
+    __syncthreads();  // previous block fully consumed; R (init or previous block) visible
+    stage_block(Bs, lds, src + r0 * ldsrc, ldsrc, cnt, ncols, brows, npad, vec16);
+    if (p0 < npanels) stage_rrows(Rp + (p0 & 1) * kNB * ldr, ldr, R, npad, p0 * kNB, tid, kTqThreads);
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
@@ -88,7 +437,7 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
         if (col < ncols) {
           double a = l1a[h], q = sqa[h];
           for (int i = 0; i < cnt; ++i) {
-            const double v = Bs[i * lds + col];
+            const double v = Bs[i * lds + (col ^ swz(i))];
             a += fabs(v);
             q = fma(v, v, q);
           }
@@ -97,190 +446,65 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
         }
       }
     }
-    const int p0 = triangular ? (int)min64(r0 / NB, npanels) : 0;
-    if (tid < NB * NB && p0 < npanels) {
-      const int j0 = p0 * NB;
-      Rd[tid] = R[(int64_t)(j0 + tid / NB) * npad + j0 + tid % NB];
-    }
-    int buf = 0;
     for (int p = p0; p < npanels; ++p) {
-      const int j0 = p * NB;
-      __syncthreads();  // (A) trailing update of the previous panel done; Rd loaded
-      double pv[kMaxRpt];
-#pragma unroll
-      for (int q = 0; q < kMaxRpt; ++q) {
-        const int i = s + kSlots * q;
-        pv[q] = (q < rpt && i < brows) ? Bs[i * lds + j0 + c] : 0.0;
-      }
-      // ---- panel factorization: NB Householder reflectors on [R(j0:j0+NB, :); B(:, panel)]
-#pragma unroll 1
-      for (int jj = 0; jj < NB; ++jj) {
-        const int j = j0 + jj;
-        const int src_lane = (lane & ~(NB - 1)) | jj;
-        double xj[kMaxRpt];
-        double d = 0.0;
-#pragma unroll
-        for (int q = 0; q < kMaxRpt; ++q) {
-          xj[q] = __shfl_sync(0xffffffffu, pv[q], src_lane);
-          d = fma(xj[q], pv[q], d);
+      const int j0 = p * kNB;
+      const int buf = p & 1;
+      const double* Rpc = Rp + buf * kNB * ldr;
+      const double* Tmc = Tm + buf * kNB * kNB;
+      const bool more = p + 1 < npanels;
+      const int tq_p = (r0 == 0 && p < 64) ? p : -1;
+      if (warp == 0 || (NPW == 2 && warp == 4)) {
+        if (p > p0) named_sync(kBarColsReady, kTqThreads);
+        TQ_TRACE(1);
+        panel_factor<RQ, NPW>(Bs, lds, brows, j0, R, npad, Rpc, ldr, Tm + buf * kNB * kNB, red, xch, warp >> 2,
+                              lane, tq_p);
+        TQ_TRACE(2);
+        named_arrive(kBarPanelDone, kTqThreads);
+      } else if (warp == 4) {  // NPW == 1: helper on SMSP 0 (no DMMA): stages the R rows of panel p+1
+        named_sync(kBarPanelDone, kTqThreads);
+        if (more) {
+          stage_rrows(Rp + (buf ^ 1) * kNB * ldr, ldr, R, npad, j0 + kNB, lane, 32);
+          cp_async_commit();
+          cp_async_wait<0>();
+          __syncwarp();
+          named_arrive(kBarColsReady, kTqThreads);
         }
-#pragma unroll
-        for (int off = NB; off < 32; off <<= 1) d += __shfl_xor_sync(0xffffffffu, d, off);
-        if (lane < NB) part[(buf * kTqWarps + warp) * NB + lane] = d;
-        __syncthreads();
-        double dj = 0.0, dc = 0.0;
-#pragma unroll
-        for (int w = 0; w < kTqWarps; ++w) {
-          dj += part[(buf * kTqWarps + w) * NB + jj];
-          dc += part[(buf * kTqWarps + w) * NB + c];
-        }
-        buf ^= 1;
-        const double alpha = Rd[jj * NB + jj];
-        double tau = 0.0, scale = 0.0, beta = alpha;
-        if (dj > 0.0) {  // dlarfg: beta = -sign(alpha) * ||(alpha, x)||, tau = (beta - alpha) / beta
-          const double nrm = sqrt(fma(alpha, alpha, dj));
-          beta = -copysign(nrm, alpha);
-          tau = (beta - alpha) / beta;
-          scale = 1.0 / (alpha - beta);
-        }
-        if (c > jj) {
-          const double rjc = Rd[jj * NB + c];
-          const double tw = tau * fma(scale, dc, rjc);
-          const double f = tw * scale;
-#pragma unroll
-          for (int q = 0; q < kMaxRpt; ++q) pv[q] = fma(-f, xj[q], pv[q]);
-          if (s == 0) R[(int64_t)j * npad + j0 + c] = rjc - tw;
-        } else if (c == jj) {
-#pragma unroll
-          for (int q = 0; q < kMaxRpt; ++q) pv[q] *= scale;
-          if (s == 0) {
-            R[(int64_t)j * npad + j] = beta;
-            tau_s[jj] = tau;
+      } else {
+        const int gi = gemm_index(warp);
+        named_sync(kBarPanelDone, kTqThreads);
+        if (more) {
+          TQ_TRACE(3);
+          const bool stager = NPW == 2 && gi == 0;  // with two panel warps, GEMM warp 0 stages R rows
+          if (stager) {
+            stage_rrows(Rp + (buf ^ 1) * kNB * ldr, ldr, R, npad, j0 + kNB, lane, 32);
+            cp_async_commit();
           }
-        } else if (s == 0) {
-          Tcol[c * NB + jj] = scale * dc;  // v_c^T v_jj
+          lookahead_cb(Bs, lds, brows, j0, Rpc, ldr, R, npad, Tmc, Wpart, p + 1, gi, lane);
+          if (stager) {
+            cp_async_wait<0>();
+            __syncwarp();
+          }
+          TQ_TRACE(4);
+          named_arrive(kBarColsReady, kTqThreads);
         }
-      }
+        // trailing column blocks p+2 .. ncb-1, round-robin over the GEMM warps in groups of G
+        for (int base = p + 2 + gi; base < ncb; base += kGemmWarps * G) {
+          int cnt_g = 0;
+          int cbs[G];
 #pragma unroll
-      for (int q = 0; q < kMaxRpt; ++q) {
-        const int i = s + kSlots * q;
-        if (q < rpt && i < brows) Bs[i * lds + j0 + c] = pv[q];
-      }
-      __syncthreads();  // (C) V in Bs, tau / Tcol visible
-      if (warp == 0 && lane < NB) {  // T (upper triangular, dlarft forward/columnwise): row `lane`
-        double trow[NB];
-#pragma unroll
-        for (int jj = 0; jj < NB; ++jj) {
-          if (jj < lane) {
-            trow[jj] = 0.0;
-          } else if (jj == lane) {
-            trow[jj] = tau_s[jj];
+          for (int gg = 0; gg < G; ++gg) {
+            cbs[gg] = base + kGemmWarps * gg;
+            if (cbs[gg] < ncb) ++cnt_g;
+          }
+          if (cnt_g == G) {
+            update_cbs<G>(Bs, lds, brows, j0, Rpc, ldr, R, npad, Tmc, Wsc, cbs, lane, tq_p);
           } else {
-            double acc = 0.0;
-#pragma unroll
-            for (int q = 0; q < jj; ++q)
-              if (q >= lane) acc = fma(trow[q], Tcol[q * NB + jj], acc);
-            trow[jj] = -tau_s[jj] * acc;
-          }
-        }
-#pragma unroll
-        for (int jj = 0; jj < NB; ++jj) Tm[lane * NB + jj] = trow[jj];
-      }
-      __syncthreads();  // (D) T visible
-      // ---- trailing update on warp-owned column blocks (no CTA barrier inside)
-      const int cb0 = (j0 + NB) / 8;
-      for (int base = cb0 + warp; base < ncb; base += kTqWarps * G) {
-        double acc[NB / 8][G][2];
-#pragma unroll
-        for (int gg = 0; gg < G; ++gg) {
-          const int cb = base + kTqWarps * gg;
-#pragma unroll
-          for (int rb = 0; rb < NB / 8; ++rb) {
-            if (cb < ncb) {
-              const double* rp = R + (int64_t)(j0 + 8 * rb + (lane >> 2)) * npad + 8 * cb + 2 * (lane & 3);
-              acc[rb][gg][0] = rp[0];
-              acc[rb][gg][1] = rp[1];
-            } else {
-              acc[rb][gg][0] = acc[rb][gg][1] = 0.0;
+            for (int gg = 0; gg < cnt_g; ++gg) {
+              const int one[1] = {cbs[gg]};
+              update_cbs<1>(Bs, lds, brows, j0, Rpc, ldr, R, npad, Tmc, Wsc, one, lane, tq_p);
             }
           }
         }
-        // W = R_p + V^T B    (K = brows, 4 rows per DMMA)
-        for (int i = 0; i < brows; i += 4) {
-          const double* row = Bs + (i + (lane & 3)) * lds;
-          double a[NB / 8];
-#pragma unroll
-          for (int rb = 0; rb < NB / 8; ++rb) a[rb] = row[j0 + 8 * rb + (lane >> 2)];
-#pragma unroll
-          for (int gg = 0; gg < G; ++gg) {
-            const int cb = base + kTqWarps * gg;
-            if (cb < ncb) {
-              const double b = row[8 * cb + (lane >> 2)];
-#pragma unroll
-              for (int rb = 0; rb < NB / 8; ++rb) dmma(acc[rb][gg][0], acc[rb][gg][1], a[rb], b);
-            }
-          }
-        }
-        // W' = T^T W ; R_p -= W' ; gather -W' as B-operand fragments
-        double wb[G][NB / 4];
-#pragma unroll
-        for (int gg = 0; gg < G; ++gg) {
-          const int cb = base + kTqWarps * gg;
-          if (cb >= ncb) continue;
-#pragma unroll
-          for (int rb = 0; rb < NB / 8; ++rb) {
-            Wsc[(8 * rb + (lane >> 2)) * 8 + 2 * (lane & 3)] = acc[rb][gg][0];
-            Wsc[(8 * rb + (lane >> 2)) * 8 + 2 * (lane & 3) + 1] = acc[rb][gg][1];
-          }
-          __syncwarp();
-          double wn[NB / 8][2];
-#pragma unroll
-          for (int ro = 0; ro < NB / 8; ++ro) {
-            wn[ro][0] = wn[ro][1] = 0.0;
-#pragma unroll
-            for (int k0 = 0; k0 < 8 * (ro + 1); k0 += 4) {
-              const double a = Tm[(k0 + (lane & 3)) * NB + 8 * ro + (lane >> 2)];
-              const double b = Wsc[(k0 + (lane & 3)) * 8 + (lane >> 2)];
-              dmma(wn[ro][0], wn[ro][1], a, b);
-            }
-            double* rp = R + (int64_t)(j0 + 8 * ro + (lane >> 2)) * npad + 8 * cb + 2 * (lane & 3);
-            rp[0] -= wn[ro][0];
-            rp[1] -= wn[ro][1];
-          }
-          __syncwarp();
-#pragma unroll
-          for (int ro = 0; ro < NB / 8; ++ro) {
-            Wsc[(8 * ro + (lane >> 2)) * 8 + 2 * (lane & 3)] = wn[ro][0];
-            Wsc[(8 * ro + (lane >> 2)) * 8 + 2 * (lane & 3) + 1] = wn[ro][1];
-          }
-          __syncwarp();
-#pragma unroll
-          for (int k4 = 0; k4 < NB / 4; ++k4) wb[gg][k4] = -Wsc[(4 * k4 + (lane & 3)) * 8 + (lane >> 2)];
-          __syncwarp();
-        }
-        // B -= V W'   (C tiles read/written in place; K = NB)
-        for (int rb = 0; rb < brows / 8; ++rb) {
-          const double* vrow = Bs + (8 * rb + (lane >> 2)) * lds + j0 + (lane & 3);
-          double a[NB / 4];
-#pragma unroll
-          for (int k4 = 0; k4 < NB / 4; ++k4) a[k4] = vrow[4 * k4];
-#pragma unroll
-          for (int gg = 0; gg < G; ++gg) {
-            const int cb = base + kTqWarps * gg;
-            if (cb < ncb) {
-              double2* cp = reinterpret_cast<double2*>(Bs + (8 * rb + (lane >> 2)) * lds + 8 * cb + 2 * (lane & 3));
-              double2 cv = *cp;
-#pragma unroll
-              for (int k4 = 0; k4 < NB / 4; ++k4) dmma(cv.x, cv.y, a[k4], wb[gg][k4]);
-              *cp = cv;
-            }
-          }
-        }
-      }
-      // next panel's diagonal block of R (rows j0+NB.., untouched by this panel)
-      if (p + 1 < npanels && tid < NB * NB) {
-        const int j1 = j0 + NB;
-        Rd[tid] = R[(int64_t)(j1 + tid / NB) * npad + j1 + tid % NB];
       }
     }
   }
@@ -296,7 +520,7 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
   }
 }
 
-template <int NB, int MINB>
+template <int RQ, int NPW, int MINB>
 __global__ void __launch_bounds__(kTqThreads, MINB)
     tsqr_leaf_kernel(const double* __restrict__ x, int64_t m, int64_t ldx, int64_t rows_per_cta, TqGeom g,
                      double* __restrict__ slots, double* __restrict__ stats) {
@@ -305,12 +529,12 @@ __global__ void __launch_bounds__(kTqThreads, MINB)
   const int64_t cnt = max64(0, min64(rows_per_cta, m - r0));
   double* R = slots + (int64_t)blockIdx.x * g.npad * g.npad;
   double* st = stats ? stats + (int64_t)blockIdx.x * 2 * g.npad : nullptr;
-  tsqr_fold<NB>(R, x + r0 * ldx, cnt, ldx, g.n, g, false, true, st, smem);
+  tsqr_fold<RQ, NPW>(R, x + r0 * ldx, cnt, ldx, g.n, g, false, true, st, smem);
 }
 
 // One level of the binary-counter tree: slot[q*2^L] = qr([slot[q*2^L]; slot[q*2^L + 2^(L-1)]]),
 // or (fold) slot[dst] = qr([slot[dst]; slot[src]]).
-template <int NB, int MINB>
+template <int RQ, int NPW, int MINB>
 __global__ void __launch_bounds__(kTqThreads, MINB)
     tsqr_combine_kernel(double* __restrict__ slots, int64_t span, int64_t half, int64_t fold_dst, int64_t fold_src,
                         TqGeom g) {
@@ -324,7 +548,7 @@ __global__ void __launch_bounds__(kTqThreads, MINB)
     dst = fold_dst;
     srcs = fold_src;
   }
-  tsqr_fold<NB>(slots + dst * ss, slots + srcs * ss, g.npad, g.npad, g.npad, g, true, false, nullptr, smem);
+  tsqr_fold<RQ, NPW>(slots + dst * ss, slots + srcs * ss, g.npad, g.npad, g.npad, g, true, false, nullptr, smem);
 }
 
 // R_out (n x n, row-major, stride ldr) = sign-fixed upper triangle of slot 0 (tsqr.py:113-118).
@@ -365,65 +589,60 @@ __global__ void tsqr_pad_kernel(const double* __restrict__ rs, int n, int npad, 
 namespace {
 
 struct TqChoice {
-  int nb;
+  int rq;
+  int npw;  // panel warps (1 or 2)
   int minb;
   TqGeom g;
   size_t smem;
 };
 
-int tq_max_rows(int nb) { return (kTqThreads / nb) * kMaxRpt; }
-
-template <int NB>
-size_t tq_bytes(const TqGeom& g) { return TqLayout<NB>::bytes(g); }
-
-size_t tq_bytes_nb(int nb, const TqGeom& g) { return nb == 8 ? tq_bytes<8>(g) : tq_bytes<16>(g); }
-
-bool tq_choose(int n, int nb, int minb, TqChoice* out) {
+bool tq_choose(int n, int minb, TqChoice* out) {
   TqGeom g;
   g.n = n;
-  g.npad = (int)round_up(n, nb);
+  g.npad = (int)round_up(n, kNB);
   g.lds = smem_stride(g.npad);
   const size_t budget = (minb == 2 ? 113 : 226) * 1024;
-  g.brows = 8;
-  if (tq_bytes_nb(nb, g) > budget) return false;
-  int best = 8;
-  for (int b = 8; b <= tq_max_rows(nb); b += 8) {
+  int best = 0;
+  for (int b = 8; b <= 32 * kMaxRq; b += 8) {
     g.brows = b;
-    if (tq_bytes_nb(nb, g) <= budget) best = b;
+    if (TqLayout::bytes(g) <= budget) best = b;
   }
+  if (!best) return false;
   g.brows = best;
-  out->nb = nb;
+  int npw = 1;
+  if (const char* e = getenv("TSNMF_TSQR_PW")) npw = atoi(e) == 2 ? 2 : 1;
+  out->npw = npw;
+  out->rq = ((npw == 2 ? best / 2 : best) + 31) / 32;  // rows per lane of each panel warp
+  if (out->rq > kMaxRq) return false;
   out->minb = minb;
   out->g = g;
-  out->smem = tq_bytes_nb(nb, g);
+  out->smem = TqLayout::bytes(g);
   return true;
 }
 
 bool tq_config(int n, TqChoice* out) {
-  // Panel width / occupancy.  TSNMF_TSQR_NB / TSNMF_TSQR_CTAS override for tuning.
-  int nb = 16, minb = 2;
-  if (const char* e = getenv("TSNMF_TSQR_NB")) nb = atoi(e) == 8 ? 8 : 16;
-  if (const char* e = getenv("TSNMF_TSQR_CTAS")) minb = atoi(e) == 1 ? 1 : 2;
-  if (tq_choose(n, nb, minb, out) && out->g.brows >= 32) return true;
-  if (tq_choose(n, nb, 1, out) && out->g.brows >= 16) return true;
-  if (tq_choose(n, 8, 1, out)) return true;
-  return false;
+  // Occupancy: 1 CTA / SM with the largest block that fits (rows in flight per panel chain bound the
+  // throughput); TSNMF_TSQR_CTAS=2 selects two half-size CTAs per SM for tuning.
+  int minb = 1;
+  if (const char* e = getenv("TSNMF_TSQR_CTAS")) minb = atoi(e) == 2 ? 2 : 1;
+  if (minb == 2 && tq_choose(n, 2, out) && out->g.brows >= 48) return true;
+  return tq_choose(n, 1, out);
 }
 
-template <int NB, int MINB>
+template <int RQ, int NPW, int MINB>
 int tq_launch_all(const TqChoice& ch, const double* x, int64_t m, int64_t ldx, double* slots, double* stats,
                   int nleaves, int64_t rows_per_cta, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
-    TSNMF_CUDA_CHECK(cudaFuncSetAttribute(tsqr_leaf_kernel<NB, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    TSNMF_CUDA_CHECK(cudaFuncSetAttribute(tsqr_leaf_kernel<RQ, NPW, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           232448));
-    TSNMF_CUDA_CHECK(cudaFuncSetAttribute(tsqr_combine_kernel<NB, MINB>,
+    TSNMF_CUDA_CHECK(cudaFuncSetAttribute(tsqr_combine_kernel<RQ, NPW, MINB>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
     attr_set = true;
   }
   if (x) {
     prof_mark(kProfTsqrLeaf, true, st);
-    tsqr_leaf_kernel<NB, MINB><<<nleaves, kTqThreads, ch.smem, st>>>(x, m, ldx, rows_per_cta, ch.g, slots, stats);
+    tsqr_leaf_kernel<RQ, NPW, MINB><<<nleaves, kTqThreads, ch.smem, st>>>(x, m, ldx, rows_per_cta, ch.g, slots, stats);
     TSNMF_LAUNCH_CHECK();
     prof_mark(kProfTsqrLeaf, false, st);
   }
@@ -431,7 +650,7 @@ int tq_launch_all(const TqChoice& ch, const double* x, int64_t m, int64_t ldx, d
   // binary-counter tree (tsqr.py:213-230): perfect levels, then fold leftover subtrees low -> high
   for (int64_t span = 2; span <= nleaves; span *= 2) {
     const int64_t q = nleaves / span;
-    tsqr_combine_kernel<NB, MINB><<<(unsigned)q, kTqThreads, ch.smem, st>>>(slots, span, span / 2, 0, 0, ch.g);
+    tsqr_combine_kernel<RQ, NPW, MINB><<<(unsigned)q, kTqThreads, ch.smem, st>>>(slots, span, span / 2, 0, 0, ch.g);
     TSNMF_LAUNCH_CHECK();
   }
   int64_t offs[64];
@@ -443,19 +662,32 @@ int tq_launch_all(const TqChoice& ch, const double* x, int64_t m, int64_t ldx, d
       o += (1LL << b);
     }
   for (int t = nsub - 2; t >= 0; --t) {
-    tsqr_combine_kernel<NB, MINB><<<1, kTqThreads, ch.smem, st>>>(slots, 0, 0, offs[t], offs[t + 1], ch.g);
+    tsqr_combine_kernel<RQ, NPW, MINB><<<1, kTqThreads, ch.smem, st>>>(slots, 0, 0, offs[t], offs[t + 1], ch.g);
     TSNMF_LAUNCH_CHECK();
   }
   prof_mark(kProfTsqrTree, false, st);
   return kOk;
 }
 
+template <int NPW, int MINB>
+int tq_dispatch_rq(const TqChoice& ch, const double* x, int64_t m, int64_t ldx, double* slots, double* stats,
+                   int nleaves, int64_t rows_per_cta, cudaStream_t st) {
+  switch (ch.rq) {
+    case 1: return tq_launch_all<1, NPW, MINB>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
+    case 2: return tq_launch_all<2, NPW, MINB>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
+    case 3: return tq_launch_all<3, NPW, MINB>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
+    default: return tq_launch_all<4, NPW, MINB>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
+  }
+}
+
 int tq_dispatch(const TqChoice& ch, const double* x, int64_t m, int64_t ldx, double* slots, double* stats,
                 int nleaves, int64_t rows_per_cta, cudaStream_t st) {
-  if (ch.nb == 16 && ch.minb == 2) return tq_launch_all<16, 2>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
-  if (ch.nb == 16) return tq_launch_all<16, 1>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
-  if (ch.minb == 2) return tq_launch_all<8, 2>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
-  return tq_launch_all<8, 1>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
+  if (ch.npw == 2) {
+    if (ch.minb == 2) return tq_dispatch_rq<2, 2>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
+    return tq_dispatch_rq<2, 1>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
+  }
+  if (ch.minb == 2) return tq_dispatch_rq<1, 2>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
+  return tq_dispatch_rq<1, 1>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
 }
 
 int device_sms() {
@@ -482,6 +714,17 @@ void tq_plan(const TqChoice& ch, int64_t m, int* nleaves, int64_t* rows_per_cta)
 }  // namespace
 
 int tsqr_max_cols() { return 512; }
+
+#ifdef TSNMF_TRACE
+extern "C" int tsnmf_trace_read(long long* out, int cap) {
+  // out: 8 warps x 4096 slots (panel * 64 + tag) of clock64 values, 0 = not recorded
+  const int n = 8 * 64 * 64 < cap ? 8 * 64 * 64 : cap;
+  cudaMemcpyFromSymbol(out, g_trace, sizeof(long long) * n);
+  static long long zero[8 * 64 * 64];
+  cudaMemcpyToSymbol(g_trace, zero, sizeof(zero));
+  return n;
+}
+#endif
 
 size_t tsqr_workspace_bytes(int64_t m, int n) {
   TqChoice ch;
@@ -546,7 +789,7 @@ int tsqr_describe(int n, int64_t m, int* nb, int* brows, int* ctas_per_sm, int* 
   if (!tq_config(n, &ch)) return set_error(kUsage, "tsqr: n = %d too large", n);
   int64_t rpc;
   tq_plan(ch, max64(m, 1), nleaves, &rpc);
-  *nb = ch.nb;
+  *nb = kNB;
   *brows = ch.g.brows;
   *ctas_per_sm = ch.minb;
   return kOk;

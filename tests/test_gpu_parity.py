@@ -15,6 +15,7 @@ from paper_1402_6964_b200 import streams
 
 pytestmark = pytest.mark.gpu
 R_TOL = 1e-10
+RANK_DEFICIENT = {"zerocol_257x25"}
 
 
 def dev(a):
@@ -79,7 +80,15 @@ def test_stream_pass_matches_reference(golden_tsqr, name, size, where):
     mk = dev if where == "device" else (lambda a: a)
     chunks = [tb.RowChunk(o, mk(x[o:o + size])) for o in range(0, x.shape[0], size)]
     res = tb.stream_pass(chunks, sketch_rows=6, seed=11)
-    assert rel_err(res.factor.entries, golden_tsqr[key + "__r"]) <= R_TOL
+    if name in RANK_DEFICIENT:
+        # an exactly-zero column makes R non-unique: the reference's own R differs by 3% between chunk
+        # sizes 1 and 257 on this input; compare what is unique (R^T R, singular values).
+        want = golden_tsqr[key + "__r"]
+        assert rel_err(res.factor.entries.T @ res.factor.entries, want.T @ want) <= 1e-12
+        np.testing.assert_allclose(np.linalg.svd(res.factor.entries, compute_uv=False),
+                                   np.linalg.svd(want, compute_uv=False), rtol=1e-10, atol=1e-12)
+    else:
+        assert rel_err(res.factor.entries, golden_tsqr[key + "__r"]) <= R_TOL
     np.testing.assert_allclose(res.stats.l1, golden_tsqr[key + "__l1"], rtol=1e-12)
     np.testing.assert_allclose(res.stats.l2, golden_tsqr[key + "__l2"], rtol=1e-12)
     assert rel_err(res.sketch.entries, golden_tsqr[key + "__sketch"]) <= 1e-12
@@ -252,7 +261,9 @@ def test_device_generator_matches_oracle(oracle, name):
     assert np.array_equal(mix, omix) and planted == oplanted
     xd = synthetic.generate(spec, row0=5000, rows=3000).cpu().numpy()
     xo = oracle.config_rows(ospec, 5000, 3000, omix)
-    assert rel_err(xd, xo) <= 1e-14
+    # the generator's transcendentals are float32 (noise; lognormal / bump W for C4 / C5): CUDA vs numpy
+    # float32 ulps; uniform W (C1) is exact up to the float32 noise term
+    assert rel_err(xd, xo) <= (1e-9 if name == "C1" else 1e-6)
     assert (xd >= 0).all()
 
 
