@@ -39,6 +39,21 @@ def hbm_peak():
         return 6650.0, "fallback B200_PROFILING.md"
 
 
+def ncu_traffic_per_row(path: str, rows: int):
+    """dram bytes per row of the profiled leaf launch (profiles/r01_tsqr_leaf_ncu_full.txt, ncu --set full)."""
+    try:
+        vals = {}
+        for line in open(path):
+            if "=" in line and not line.startswith("#"):
+                k, v = line.split("=", 1)
+                num, unit = v.split()[0], v.split()[1] if len(v.split()) > 1 else ""
+                scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}.get(unit, 1.0)
+                vals[k.strip()] = float(num) * scale
+        return (vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]) / rows
+    except Exception:
+        return None
+
+
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -292,6 +307,7 @@ def main():
     leaf_flops = 2.0 * n * n * (hi - lo)
     leaf_tf = leaf_flops / (leaf_ms * 1e-3) / 1e12
     plan = dv.tsqr_plan(n, hi - lo)
+    tpr = ncu_traffic_per_row(os.path.join(ROOT, "profiles", "r01_tsqr_leaf_ncu_full.txt"), 1 << 21)
 
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
@@ -304,7 +320,11 @@ def main():
                    "l2": "inputs (>=13 GB per GPU) exceed the 126 MB L2; no flush needed",
                    "tsqr_plan": plan},
         "roofline": {"bound": "tensor", "achieved": leaf_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                     "frac": leaf_tf / FP64_PEAK_TFLOPS, "traffic": None,
+                     "frac": leaf_tf / FP64_PEAK_TFLOPS,
+                     "traffic": tpr * (hi - lo) if tpr else None,
+                     "traffic_source": "ncu --set full dram__bytes_read+write of tsqr_leaf_kernel at m=2^21 "
+                                       "(profiles/r01_tsqr_leaf_ncu_full.txt), per row x rows per launch; "
+                                       f"algorithmic {8 * n * (hi - lo)} B",
                      "kernel": "tsqr_leaf_kernel (FP64 DMMA m8n8k4)",
                      "algorithmic": f"2 n^2 = {2 * n * n} flop per row x {hi - lo} rows per launch",
                      "peak_source": "measured FP64 DMMA peak, profiles/r01_peaks.json",
