@@ -119,6 +119,45 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+// XOR swizzle of shared-memory row blocks (stride % 16 == 8 doubles): column c of row r lives at
+// r*lds + swz_col(r, c).  Makes the DMMA operand slabs (lane: row l%4, col l/4), V fragments
+// (row l/4, col l%4) and 16-byte C-tile rows (row l/4, col 2*(l%4)) conflict-free; XOR by 0 or 4 stays
+// inside aligned 8-column groups so 16-byte pairs are preserved.
+__host__ __device__ __forceinline__ int swz_row(int row) { return (row & 2) << 1; }
+__host__ __device__ __forceinline__ int swz_col(int row, int col) { return col ^ swz_row(row); }
+
+// Swizzled variant of stage_rows below (same contract; cols_total must be a multiple of 8).
+__device__ __forceinline__ void stage_rows_swz(double* __restrict__ dst, int lds, const double* __restrict__ src,
+                                               int64_t ldsrc, int nrows, int ncols, int rows_total,
+                                               int cols_total, bool vec16) {
+  const int tid = threadIdx.x, nth = blockDim.x;
+  if (vec16) {
+    const int pairs = ncols >> 1;
+    for (int idx = tid; idx < nrows * pairs; idx += nth) {
+      const int r = idx / pairs, c = (idx - r * pairs) * 2;
+      cp_async16(dst + (int64_t)r * lds + swz_col(r, c), src + r * ldsrc + c);
+    }
+    if (ncols & 1)
+      for (int r = tid; r < nrows; r += nth)
+        cp_async8(dst + (int64_t)r * lds + swz_col(r, ncols - 1), src + r * ldsrc + ncols - 1);
+  } else {
+    for (int idx = tid; idx < nrows * ncols; idx += nth) {
+      const int r = idx / ncols, c = idx - r * ncols;
+      cp_async8(dst + (int64_t)r * lds + swz_col(r, c), src + r * ldsrc + c);
+    }
+  }
+  const int pad = cols_total - ncols;
+  if (pad > 0)
+    for (int idx = tid; idx < nrows * pad; idx += nth) {
+      const int r = idx / pad, c = ncols + (idx - r * pad);
+      dst[(int64_t)r * lds + swz_col(r, c)] = 0.0;
+    }
+  for (int idx = tid; idx < (rows_total - nrows) * cols_total; idx += nth) {
+    const int r = nrows + idx / cols_total, c = idx % cols_total;
+    dst[(int64_t)r * lds + c] = 0.0;
+  }
+}
+
 // Stage rows [0, nrows) x cols [0, ncols) of a row-major global matrix into shared memory with
 // row stride lds; rows [nrows, rows_total) and cols [ncols, cols_total) are zero-filled.
 // All threads of the CTA participate.  Caller commits / waits.

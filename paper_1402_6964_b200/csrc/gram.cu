@@ -16,15 +16,16 @@ namespace tsnmf {
 
 constexpr int kGrThreads = 256;
 constexpr int kGrWarps = kGrThreads / 32;
-constexpr int kGrSpw = 6;                       // super-tiles per warp
-constexpr int kGrSpc = kGrWarps * kGrSpw;       // super-tiles per CTA (tile group)
-constexpr int kGrBrMax = 32;                    // rows per stage (16 when a 32-row double buffer does not fit)
+constexpr int kGrSpw = 12;   // super-tiles per warp (96 accumulator doubles)
+constexpr int kGrBrMax = 64; // rows per stage (halved until the double buffer fits)
 
 struct GrGeom {
   int n, npad;  // npad = round_up(n, 16)
-  int lds;      // smem stride
+  int lds;      // smem stride (% 16 == 8, swizzled)
   int ns;       // super-blocks per side (npad / 16)
   int nst;      // super-tiles in the upper triangle
+  int ks;       // k-slices per CTA (warps sharing a super-tile set, splitting the rows)
+  int spc;      // super-tiles per CTA (tile group) = (8 / ks) * kGrSpw
   int groups;   // tile groups
   int br;       // rows per stage
   int64_t rows_per_split;
@@ -41,7 +42,10 @@ __host__ __device__ inline void st_coords(int idx, int ns, int* P, int* Q) {
   *Q = p + rem;
 }
 
-__global__ void __launch_bounds__(kGrThreads, 2)
+// Warp w = kslice + ks * wi: k-slice `kslice` takes the 4-row k-steps i/4 = kslice (mod ks); warp index
+// wi within the slice owns a contiguous run of kGrSpw super-tiles (consecutive super-tiles mostly share
+// their row P, so the A fragments are reused).  Partials: [split][kslice][supertile][16][16].
+__global__ void __launch_bounds__(kGrThreads, 1)
     gram_kernel(const double* __restrict__ x, int64_t m, int64_t ldx, GrGeom g, double* __restrict__ partial,
                 double* __restrict__ l1part) {
   extern __shared__ __align__(16) double smem[];
@@ -50,21 +54,20 @@ __global__ void __launch_bounds__(kGrThreads, 2)
   const int64_t split = blockIdx.y;
   const int64_t rbeg = split * g.rows_per_split;
   const int64_t rend = min64(m, rbeg + g.rows_per_split);
-  const int lds = g.lds;
-  double* buf[2] = {smem, smem + g.br * lds};
-  const int br = g.br;
+  const int lds = g.lds, br = g.br, ks = g.ks;
+  const int kslice = warp % ks, wi = warp / ks;
+  double* buf[2] = {smem, smem + br * lds};
   const bool vec16 = ((ldx & 1) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
 
-  int stP[kGrSpw], stQ[kGrSpw];
-  bool stv[kGrSpw];
+  // packed super-tile coordinates: (16 P) << 16 | 16 Q; the first nvalid are real
+  int stPQ[kGrSpw];
+  const int first = group * g.spc + wi * kGrSpw;
+  const int nvalid = max(0, min(kGrSpw, g.nst - first));
 #pragma unroll
   for (int u = 0; u < kGrSpw; ++u) {
-    const int idx = group * kGrSpc + warp * kGrSpw + u;  // contiguous run: shared P fragments
-    stv[u] = idx < g.nst;
     int P = 0, Q = 0;
-    if (stv[u]) st_coords(idx, g.ns, &P, &Q);
-    stP[u] = P;
-    stQ[u] = Q;
+    if (u < nvalid) st_coords(first + u, g.ns, &P, &Q);
+    stPQ[u] = (16 * P) << 16 | (16 * Q);
   }
   double acc[kGrSpw][4][2];
 #pragma unroll
@@ -73,17 +76,17 @@ __global__ void __launch_bounds__(kGrThreads, 2)
     for (int t = 0; t < 4; ++t) acc[u][t][0] = acc[u][t][1] = 0.0;
   double l1a[2] = {0.0, 0.0};
   const bool do_l1 = (group == 0) && (l1part != nullptr);
+  const int frag_col = (lane >> 2) ^ ((lane & 2) << 1);  // swizzled slab fragment: row i + l%4, col l/4
 
-  const int64_t nstages = ceil_div(max64(rend - rbeg, 0), g.br);
+  const int64_t nstages = ceil_div(max64(rend - rbeg, 0), br);
   if (nstages > 0) {
-    stage_rows(buf[0], lds, x + rbeg * ldx, ldx, (int)min64(g.br, rend - rbeg), g.n, g.br, g.npad, vec16);
+    stage_rows_swz(buf[0], lds, x + rbeg * ldx, ldx, (int)min64(br, rend - rbeg), g.n, br, g.npad, vec16);
     cp_async_commit();
   }
   for (int64_t s = 0; s < nstages; ++s) {
     if (s + 1 < nstages) {
-      const int64_t r0 = rbeg + (s + 1) * g.br;
-      stage_rows(buf[(s + 1) & 1], lds, x + r0 * ldx, ldx, (int)min64(g.br, rend - r0), g.n, g.br,
-                 g.npad, vec16);
+      const int64_t r0 = rbeg + (s + 1) * br;
+      stage_rows_swz(buf[(s + 1) & 1], lds, x + r0 * ldx, ldx, (int)min64(br, rend - r0), g.n, br, g.npad, vec16);
       cp_async_commit();
       cp_async_wait<1>();
     } else {
@@ -97,35 +100,37 @@ __global__ void __launch_bounds__(kGrThreads, 2)
         const int col = tid + h * kGrThreads;
         if (col < g.n) {
           double a = l1a[h];
-#pragma unroll 8
-          for (int i = 0; i < br; ++i) a += fabs(xs[i * lds + col]);
+          for (int i = 0; i < br; ++i) a += fabs(xs[i * lds + swz_col(i, col)]);
           l1a[h] = a;
         }
       }
     }
-#pragma unroll 2
-    for (int i = 0; i < br; i += 4) {
-      const double* row = xs + (i + (lane & 3)) * lds + (lane >> 2);
+#pragma unroll 1
+    for (int i = 4 * kslice; i < br; i += 4 * ks) {
+      const double* row = xs + (i + (lane & 3)) * lds + frag_col;
+      double a0 = 0.0, a1 = 0.0;
 #pragma unroll
       for (int u = 0; u < kGrSpw; ++u) {
-        if (!stv[u]) continue;
-        const int P = stP[u], Q = stQ[u];
-        const double a0 = row[16 * P], a1 = row[16 * P + 8];
-        const double b0 = row[16 * Q], b1 = row[16 * Q + 8];
+        if (u >= nvalid) break;
+        const int P16 = stPQ[u] >> 16, Q16 = stPQ[u] & 0xffff;
+        if (u == 0 || P16 != (stPQ[u > 0 ? u - 1 : 0] >> 16)) {
+          a0 = row[P16];
+          a1 = row[P16 + 8];
+        }
+        const double b0 = row[Q16], b1 = row[Q16 + 8];
         dmma(acc[u][0][0], acc[u][0][1], a0, b0);
         dmma(acc[u][1][0], acc[u][1][1], a0, b1);
         dmma(acc[u][3][0], acc[u][3][1], a1, b1);
-        if (P != Q) dmma(acc[u][2][0], acc[u][2][1], a1, b0);
+        if (P16 != Q16) dmma(acc[u][2][0], acc[u][2][1], a1, b0);
       }
     }
     __syncthreads();  // buffer reuse
   }
-  // partial layout: [split][supertile][16][16]
 #pragma unroll
   for (int u = 0; u < kGrSpw; ++u) {
-    if (!stv[u]) continue;
-    const int idx = group * kGrSpc + warp * kGrSpw + u;
-    double* dst = partial + (split * g.nst + idx) * 256;
+    if (u >= nvalid) break;
+    const int idx = first + u;
+    double* dst = partial + ((split * ks + kslice) * g.nst + idx) * 256;
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       const int ti = t >> 1, tj = t & 1;
@@ -153,7 +158,7 @@ __global__ void gram_reduce_kernel(const double* __restrict__ partial, int64_t s
     idx += Q - P;
     const int64_t off = (int64_t)idx * 256 + (i % 16) * 16 + (j % 16);
     double acc = 0.0;
-    for (int64_t s = 0; s < splits; ++s) acc += partial[s * g.nst * 256 + off];
+    for (int64_t s = 0; s < splits * g.ks; ++s) acc += partial[s * g.nst * 256 + off];
     out[(int64_t)i * ldg + j] = acc;
     out[(int64_t)j * ldg + i] = acc;
     if (i == j && sumsq) sumsq[i] = acc;
@@ -178,9 +183,13 @@ GrGeom gr_geom(int64_t m, int n, int sms) {
   g.lds = smem_stride(g.npad);
   g.ns = g.npad / 16;
   g.nst = g.ns * (g.ns + 1) / 2;
-  g.groups = (int)ceil_div(g.nst, kGrSpc);
-  g.br = (2 * kGrBrMax * g.lds * 8 <= 227 * 1024) ? kGrBrMax : kGrBrMax / 2;
-  const int64_t target = max64(1, (int64_t)2 * sms / g.groups);
+  g.ks = 8;  // k-slices: as many as keep every warp busy
+  while (g.ks > 1 && (kGrWarps / g.ks) * kGrSpw < g.nst) g.ks /= 2;
+  g.spc = (kGrWarps / g.ks) * kGrSpw;
+  g.groups = (int)ceil_div(g.nst, g.spc);
+  g.br = kGrBrMax;
+  while (g.br > 8 && 2 * g.br * g.lds * 8 > 227 * 1024) g.br /= 2;
+  const int64_t target = max64(1, (int64_t)sms / g.groups);
   const int64_t splits = max64(1, min64(target, ceil_div(m, 4 * g.br)));
   g.rows_per_split = round_up(ceil_div(m, splits), g.br);
   return g;
@@ -205,7 +214,7 @@ size_t gram_workspace_bytes(int64_t m, int n) {
   if (n < 1 || n > gram_max_cols()) return 0;
   GrGeom g = gr_geom(max64(m, 1), n, sm_count());
   const int64_t splits = gr_splits(max64(m, 1), g);
-  return sizeof(double) * (size_t)(splits * g.nst * 256 + splits * g.npad) + 256;
+  return sizeof(double) * (size_t)(splits * g.ks * g.nst * 256 + splits * g.npad) + 256;
 }
 
 int gram_run(const double* x, int64_t m, int n, int64_t ldx, double* gout, int64_t ldg, double* l1, double* sumsq,
@@ -213,10 +222,10 @@ int gram_run(const double* x, int64_t m, int n, int64_t ldx, double* gout, int64
   if (n > gram_max_cols()) return set_error(kUsage, "gram: n = %d exceeds %d", n, gram_max_cols());
   GrGeom g = gr_geom(m, n, sm_count());
   const int64_t splits = gr_splits(m, g);
-  const size_t need = sizeof(double) * (size_t)(splits * g.nst * 256 + splits * g.npad);
+  const size_t need = sizeof(double) * (size_t)(splits * g.ks * g.nst * 256 + splits * g.npad);
   if (ws_bytes < need) return set_error(kUsage, "gram: workspace too small (%zu < %zu bytes)", ws_bytes, need);
   double* partial = reinterpret_cast<double*>(ws);
-  double* l1part = partial + splits * g.nst * 256;
+  double* l1part = partial + splits * g.ks * g.nst * 256;
   const size_t smem = gr_smem(g);
   static bool attr = false;
   if (!attr) {
