@@ -56,7 +56,6 @@ __global__ void __launch_bounds__(kGrThreads, 1)
   const int64_t rend = min64(m, rbeg + g.rows_per_split);
   const int lds = g.lds, br = g.br, ks = g.ks;
   const int kslice = warp % ks, wi = warp / ks;
-  double* buf[2] = {smem, smem + br * lds};
   const bool vec16 = ((ldx & 1) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
 
   // packed super-tile coordinates: (16 P) << 16 | 16 Q; the first nvalid are real
@@ -80,20 +79,21 @@ __global__ void __launch_bounds__(kGrThreads, 1)
 
   const int64_t nstages = ceil_div(max64(rend - rbeg, 0), br);
   if (nstages > 0) {
-    stage_rows_swz(buf[0], lds, x + rbeg * ldx, ldx, (int)min64(br, rend - rbeg), g.n, br, g.npad, vec16);
+    stage_rows_swz(smem, lds, x + rbeg * ldx, ldx, (int)min64(br, rend - rbeg), g.n, br, g.npad, vec16);
     cp_async_commit();
   }
   for (int64_t s = 0; s < nstages; ++s) {
     if (s + 1 < nstages) {
       const int64_t r0 = rbeg + (s + 1) * br;
-      stage_rows_swz(buf[(s + 1) & 1], lds, x + r0 * ldx, ldx, (int)min64(br, rend - r0), g.n, br, g.npad, vec16);
+      stage_rows_swz(smem + ((s + 1) & 1) * br * lds, lds, x + r0 * ldx, ldx, (int)min64(br, rend - r0), g.n, br,
+                     g.npad, vec16);
       cp_async_commit();
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
     __syncthreads();
-    const double* xs = buf[s & 1];
+    const double* xs = smem + (s & 1) * br * lds;
     if (do_l1) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -105,23 +105,20 @@ __global__ void __launch_bounds__(kGrThreads, 1)
         }
       }
     }
+    // branch-free DMMA issue: padding super-tiles (u >= nvalid) compute on (0, 0) and are not stored;
+    // diagonal super-tiles also form their (unused) lower tile
 #pragma unroll 1
     for (int i = 4 * kslice; i < br; i += 4 * ks) {
       const double* row = xs + (i + (lane & 3)) * lds + frag_col;
-      double a0 = 0.0, a1 = 0.0;
 #pragma unroll
       for (int u = 0; u < kGrSpw; ++u) {
-        if (u >= nvalid) break;
         const int P16 = stPQ[u] >> 16, Q16 = stPQ[u] & 0xffff;
-        if (u == 0 || P16 != (stPQ[u > 0 ? u - 1 : 0] >> 16)) {
-          a0 = row[P16];
-          a1 = row[P16 + 8];
-        }
+        const double a0 = row[P16], a1 = row[P16 + 8];
         const double b0 = row[Q16], b1 = row[Q16 + 8];
         dmma(acc[u][0][0], acc[u][0][1], a0, b0);
         dmma(acc[u][1][0], acc[u][1][1], a0, b1);
+        dmma(acc[u][2][0], acc[u][2][1], a1, b0);
         dmma(acc[u][3][0], acc[u][3][1], a1, b1);
-        if (P16 != Q16) dmma(acc[u][2][0], acc[u][2][1], a1, b0);
       }
     }
     __syncthreads();  // buffer reuse

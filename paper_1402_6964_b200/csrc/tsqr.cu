@@ -292,35 +292,33 @@ __device__ __forceinline__ void update_cbs(double* __restrict__ Bs, int lds, int
     __syncwarp();
   }
   TQ_TRACE(22);
-  // B -= V W'   (C tiles read/written in place; K = 8), two row blocks per iteration
+  // B -= V W'   (C tiles read/written in place; K = 8), two row blocks per iteration (brows % 16 == 0)
 #pragma unroll 1
   for (int rb = 0; rb < brows / 8; rb += 2) {
     double* rowa = Bs + (8 * rb + (lane >> 2)) * lds;
     double* rowb = rowa + 8 * lds;
-    const bool two = rb + 1 < brows / 8;
     const double a0 = rowa[j0 + ((lane & 3) ^ vsw)], a1 = rowa[j0 + ((4 + (lane & 3)) ^ vsw)];
-    const double b0 = two ? rowb[j0 + ((lane & 3) ^ vsw)] : 0.0;
-    const double b1 = two ? rowb[j0 + ((4 + (lane & 3)) ^ vsw)] : 0.0;
+    const double b0 = rowb[j0 + ((lane & 3) ^ vsw)], b1 = rowb[j0 + ((4 + (lane & 3)) ^ vsw)];
     double2 ca[G], cb2[G];
 #pragma unroll
     for (int gg = 0; gg < G; ++gg) {
       ca[gg] = *reinterpret_cast<const double2*>(rowa + 8 * cbs[gg] + ((2 * (lane & 3)) ^ vsw));
-      if (two) cb2[gg] = *reinterpret_cast<const double2*>(rowb + 8 * cbs[gg] + ((2 * (lane & 3)) ^ vsw));
+      cb2[gg] = *reinterpret_cast<const double2*>(rowb + 8 * cbs[gg] + ((2 * (lane & 3)) ^ vsw));
     }
 #pragma unroll
     for (int gg = 0; gg < G; ++gg) {
       dmma(ca[gg].x, ca[gg].y, a0, wb[gg][0]);
-      if (two) dmma(cb2[gg].x, cb2[gg].y, b0, wb[gg][0]);
+      dmma(cb2[gg].x, cb2[gg].y, b0, wb[gg][0]);
     }
 #pragma unroll
     for (int gg = 0; gg < G; ++gg) {
       dmma(ca[gg].x, ca[gg].y, a1, wb[gg][1]);
-      if (two) dmma(cb2[gg].x, cb2[gg].y, b1, wb[gg][1]);
+      dmma(cb2[gg].x, cb2[gg].y, b1, wb[gg][1]);
     }
 #pragma unroll
     for (int gg = 0; gg < G; ++gg) {
       *reinterpret_cast<double2*>(rowa + 8 * cbs[gg] + ((2 * (lane & 3)) ^ vsw)) = ca[gg];
-      if (two) *reinterpret_cast<double2*>(rowb + 8 * cbs[gg] + ((2 * (lane & 3)) ^ vsw)) = cb2[gg];
+      *reinterpret_cast<double2*>(rowb + 8 * cbs[gg] + ((2 * (lane & 3)) ^ vsw)) = cb2[gg];
     }
   }
   TQ_TRACE(23);
@@ -603,7 +601,7 @@ bool tq_choose(int n, int minb, TqChoice* out) {
   g.lds = smem_stride(g.npad);
   const size_t budget = (minb == 2 ? 113 : 226) * 1024;
   int best = 0;
-  for (int b = 8; b <= 32 * kMaxRq; b += 8) {
+  for (int b = 16; b <= 32 * kMaxRq; b += 16) {  // multiple of 16: B -= V W' runs row-block pairs
     g.brows = b;
     if (TqLayout::bytes(g) <= budget) best = b;
   }
