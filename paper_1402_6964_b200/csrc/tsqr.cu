@@ -34,8 +34,8 @@ struct TqGeom {
 
 struct TqLayout {
   // offsets in doubles from the dynamic smem base
-  __host__ __device__ static int rp(const TqGeom& g) { return g.brows * g.lds; }            // 2 x 8 R rows (stride lds)
-  __host__ __device__ static int tm(const TqGeom& g) { return rp(g) + 2 * kNB * g.lds; }    // 2 x 8x8 T
+  __host__ __device__ static int rd(const TqGeom& g) { return g.brows * g.lds; }            // 2 x 8x8 R diag blocks
+  __host__ __device__ static int tm(const TqGeom& g) { return rd(g) + 2 * kNB * kNB; }      // 2 x 8x8 T
   __host__ __device__ static int red(const TqGeom& g) { return tm(g) + 2 * kNB * kNB; }    // 2 x 32 x 9 partials
   __host__ __device__ static int xch(const TqGeom& g) { return red(g) + 2 * 32 * 9; }       // 2 x 16 exchange
   __host__ __device__ static int wsc(const TqGeom& g) { return xch(g) + 32; }                // per-warp 8x8 scratch
@@ -63,6 +63,14 @@ __device__ __forceinline__ void named_sync(int id, int count) {
 __device__ __forceinline__ void named_arrive(int id, int count) {
   asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
 }
+// trace builds: force a deferred-blocking barrier to resolve before the next trace point
+#ifdef TSNMF_TRACE
+#define TQ_RESOLVE(smem_ptr) (void)(*(volatile double*)(smem_ptr))
+#else
+#define TQ_RESOLVE(smem_ptr) \
+  do {                       \
+  } while (0)
+#endif
 __device__ __forceinline__ int gemm_index(int warp) { return warp < 4 ? warp - 1 : warp - 2; }  // 0..5
 
 #ifdef TSNMF_TRACE
@@ -89,13 +97,42 @@ __device__ long long g_trace[8][64 * 64];
 // compute identical reflectors).  Reflector (dlarfg convention): beta = -sign(alpha) ||(alpha, x)||,
 // tau = (beta - alpha)/beta, v = x/(alpha - beta).  T (upper triangular, dlarft forward columnwise) is
 // built incrementally off the critical path; R row entries are kept in registers (lane c owns column
-// c) and stored once per panel.  Rd: the 8 R rows of this panel staged in shared memory (stride ldr).
+// c) and stored once per panel.  Rd: the 8x8 diagonal block of R for this panel, staged in shared memory.
 constexpr int kBarPanelPair = 4;
+#ifndef TSNMF_LAZY_PANEL
+#define TSNMF_LAZY_PANEL 1
+#endif
+constexpr bool kLazyPanel = TSNMF_LAZY_PANEL != 0;
+#ifndef TSNMF_HELPER_LOOKAHEAD
+#define TSNMF_HELPER_LOOKAHEAD 1
+#endif
+constexpr bool kHelperLookahead = TSNMF_HELPER_LOOKAHEAD != 0;
+
+// 1/sqrt(a) and 1/a for the Householder scalars: hardware approximation + Newton steps (each doubles the
+// correct bits: ~23 -> ~46 -> full), accurate to ~1 ulp; outside [2^-900, 2^900] (where the .ftz
+// approximation would flush) the IEEE library versions are used.  a > 0 here.
+__device__ __forceinline__ double fast_rsqrt(double a) {
+  if (!(a > 0x1p-900 && a < 0x1p+900)) return rsqrt(a);  // denormal / extreme range: IEEE path
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+  const double h = 0.5 * a;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return y;
+}
+__device__ __forceinline__ double fast_rcp(double a) {
+  if (!(a > 0x1p-900 && a < 0x1p+900)) return __drcp_rn(a);
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+  y = y * fma(-a, y, 2.0);
+  y = y * fma(-a, y, 2.0);
+  return y;
+}
 
 template <int RQ, int NPW>
 __device__ __forceinline__ void panel_factor(double* __restrict__ Bs, int lds, int brows, int j0,
                                              double* __restrict__ R, int npad, const double* __restrict__ Rd,
-                                             int ldr, double* __restrict__ Tm, double* __restrict__ red,
+                                             double* __restrict__ Tm, double* __restrict__ red,
                                              double* __restrict__ xch, int h, int lane, int tq_p) {
   const int half = NPW == 2 ? (brows + 1) / 2 : brows;
   const int row0 = h * half;
@@ -105,8 +142,14 @@ __device__ __forceinline__ void panel_factor(double* __restrict__ Bs, int lds, i
 #pragma unroll
   for (int q = 0; q < RQ; ++q) {
     const int rl = lane + 32 * q;
+    const double* rp = Bs + (row0 + rl) * lds + j0;
 #pragma unroll
-    for (int c = 0; c < kNB; ++c) x[q][c] = (rl < rows_mine) ? Bs[(row0 + rl) * lds + j0 + (c ^ sw)] : 0.0;
+    for (int c = 0; c < kNB; c += 2) {  // 16-byte accesses: swizzle keeps (c, c+1) pairs adjacent
+      double2 v = make_double2(0.0, 0.0);
+      if (rl < rows_mine) v = *reinterpret_cast<const double2*>(rp + (c ^ sw));
+      x[q][c] = v.x;
+      x[q][c + 1] = v.y;
+    }
   }
   double trow[kNB], rmine[kNB];
 #pragma unroll
@@ -143,20 +186,20 @@ __device__ __forceinline__ void panel_factor(double* __restrict__ Bs, int lds, i
       for (int c = 0; c < kNB; ++c) d[c] = __shfl_sync(0xffffffffu, tot, c);
     }
     TQ_TRACE(30 + jj);
-    const double alpha = Rd[jj * ldr + j0 + jj];
+    const double alpha = Rd[jj * kNB + jj];
     double tau = 0.0, scale = 0.0, beta = alpha;
     if (d[jj] > 0.0) {
       // inv = 1/||(alpha, x)||;  tau = (beta - alpha)/beta = 1 + |alpha| inv;  scale = sign(alpha)/(|alpha| + nrm)
       const double ss = fma(alpha, alpha, d[jj]);
-      const double inv = rsqrt(ss);
+      const double inv = fast_rsqrt(ss);
       const double nrm = ss * inv;
       beta = -copysign(nrm, alpha);
       tau = fma(fabs(alpha), inv, 1.0);
-      scale = copysign(__drcp_rn(fabs(alpha) + nrm), alpha);
+      scale = copysign(fast_rcp(fabs(alpha) + nrm), alpha);
     }
 #pragma unroll
     for (int c = jj + 1; c < kNB; ++c) {
-      const double rjc = Rd[jj * ldr + j0 + c];
+      const double rjc = Rd[jj * kNB + c];
       const double tw = tau * fma(scale, d[c], rjc);
       const double f = tw * scale;
 #pragma unroll
@@ -178,12 +221,149 @@ __device__ __forceinline__ void panel_factor(double* __restrict__ Bs, int lds, i
   for (int q = 0; q < RQ; ++q) {
     const int rl = lane + 32 * q;
     if (rl < rows_mine) {
+      double* rp = Bs + (row0 + rl) * lds + j0;
 #pragma unroll
-      for (int c = 0; c < kNB; ++c) Bs[(row0 + rl) * lds + j0 + (c ^ sw)] = x[q][c];
+      for (int c = 0; c < kNB; c += 2) *reinterpret_cast<double2*>(rp + (c ^ sw)) = make_double2(x[q][c], x[q][c + 1]);
     }
   }
   if (h == 0 && lane < kNB) {
     double* Rcol = R + (int64_t)j0 * npad + j0 + lane;  // lane c writes R(j0 + jj, j0 + c), jj <= c
+#pragma unroll
+    for (int jj = 0; jj < kNB; ++jj)
+      if (jj <= lane) Rcol[(int64_t)jj * npad] = rmine[jj];
+#pragma unroll
+    for (int c = 0; c < kNB; ++c) Tm[lane * kNB + c] = trow[c];
+  }
+}
+
+// Single-warp panel with LAZY trailing updates (the NPW == 1 path).  Step s (column j0 + s):
+//   * only the next pivot column is updated eagerly:  x_s -= f_s * u_{s-1}   (u = previous pivot, unscaled)
+//   * dot products P_c = x_s . x_c use the trailing columns BEFORE step s-1's update, then are corrected
+//     d_c = P_c - f_c * P_{s-1}  (x_c' = x_c - f_c u_{s-1});  P_{s-1} = x_s . u_{s-1} also gives the T dot
+//     v_{s-1}^T x_s = scale_{s-1} P_{s-1};
+//   * the pending trailing updates and the scaling u_{s-1} -> v_{s-1} run off the critical path, after the
+//     dots have been issued.
+// The critical path per column is: scalars -> one column update -> dots -> warp reduction -> corrections.
+// Rounding: the corrected dots carry errors O(eps |x_s| |x_c|) (x_c = the column before the last update),
+// the same order as Householder QR's normwise backward error; the parity suite checks R to 1e-10.
+template <int RQ>
+__device__ __forceinline__ void panel_factor_lazy(double* __restrict__ Bs, int lds, int brows, int j0,
+                                                  double* __restrict__ R, int npad, const double* __restrict__ Rd,
+                                                  double* __restrict__ Tm, double* __restrict__ red, int lane,
+                                                  int tq_p) {
+  const int sw = swz(lane);
+  double x[RQ][kNB];
+#pragma unroll
+  for (int q = 0; q < RQ; ++q) {
+    const int rl = lane + 32 * q;
+    const double* rp = Bs + rl * lds + j0;
+#pragma unroll
+    for (int c = 0; c < kNB; c += 2) {
+      double2 v = make_double2(0.0, 0.0);
+      if (rl < brows) v = *reinterpret_cast<const double2*>(rp + (c ^ sw));
+      x[q][c] = v.x;
+      x[q][c + 1] = v.y;
+    }
+  }
+  double trow[kNB], rmine[kNB], f[kNB];
+#pragma unroll
+  for (int c = 0; c < kNB; ++c) trow[c] = rmine[c] = f[c] = 0.0;
+  const int rc = lane & 7, rq = lane >> 3;
+  double scale_prev = 0.0;
+  // dots of step 0
+#pragma unroll
+  for (int c = 0; c < kNB; ++c) {
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < RQ; ++q) acc = fma(x[q][0], x[q][c], acc);
+    red[lane * 9 + c] = acc;
+  }
+#pragma unroll
+  for (int js = 0; js < kNB; ++js) {
+    TQ_TRACE(10 + js);
+    // (A) warp reduction of this step's dots
+    __syncwarp();
+    const double s0 = red[(rq * 8 + 0) * 9 + rc] + red[(rq * 8 + 1) * 9 + rc];
+    const double s1 = red[(rq * 8 + 2) * 9 + rc] + red[(rq * 8 + 3) * 9 + rc];
+    const double s2 = red[(rq * 8 + 4) * 9 + rc] + red[(rq * 8 + 5) * 9 + rc];
+    const double s3 = red[(rq * 8 + 6) * 9 + rc] + red[(rq * 8 + 7) * 9 + rc];
+    double tot = (s0 + s1) + (s2 + s3);
+    tot += __shfl_xor_sync(0xffffffffu, tot, 8);
+    tot += __shfl_xor_sync(0xffffffffu, tot, 16);
+    double d[kNB];
+#pragma unroll
+    for (int c = 0; c < kNB; ++c) d[c] = __shfl_sync(0xffffffffu, tot, c);
+    __syncwarp();  // red free for the next step's dots
+    TQ_TRACE(30 + js);
+    // (B) corrections for the lazily updated trailing columns; T dot of the previous pivot
+    if (js > 0) {
+#pragma unroll
+      for (int c = js + 1; c < kNB; ++c) d[c] = fma(-f[c], d[js - 1], d[c]);
+      d[js - 1] *= scale_prev;
+    }
+    // (C) reflector scalars
+    const double alpha = Rd[js * kNB + js];
+    double tau = 0.0, scale = 0.0, beta = alpha;
+    if (d[js] > 0.0) {
+      const double ss = fma(alpha, alpha, d[js]);
+      const double inv = fast_rsqrt(ss);
+      const double nrm = ss * inv;
+      beta = -copysign(nrm, alpha);
+      tau = fma(fabs(alpha), inv, 1.0);
+      scale = copysign(fast_rcp(fabs(alpha) + nrm), alpha);
+    }
+    // (D) critical: next pivot's factor, eager update of the next pivot column, next step's dots
+    if (js + 1 < kNB) {
+      const double rjn = Rd[js * kNB + js + 1];
+      const double twn = tau * fma(scale, d[js + 1], rjn);
+      f[js + 1] = twn * scale;
+      if (lane == js + 1) rmine[js] = rjn - twn;
+#pragma unroll
+      for (int q = 0; q < RQ; ++q) x[q][js + 1] = fma(-f[js + 1], x[q][js], x[q][js + 1]);
+#pragma unroll
+      for (int c = 0; c < kNB; ++c) {
+        double acc = 0.0;
+#pragma unroll
+        for (int q = 0; q < RQ; ++q) acc = fma(x[q][js + 1], x[q][c], acc);
+        red[lane * 9 + c] = acc;
+      }
+    }
+    // (E) off the critical path: remaining factors, R row, T row, pending trailing updates, u -> v
+#pragma unroll
+    for (int c = js + 2; c < kNB; ++c) {
+      const double rjc = Rd[js * kNB + c];
+      const double tw = tau * fma(scale, d[c], rjc);
+      f[c] = tw * scale;
+      if (lane == c) rmine[js] = rjc - tw;
+    }
+    if (lane == js) rmine[js] = beta;
+    {  // T[r][js] = -tau_js * sum_{q=r}^{js-1} T[r][q] (v_q^T v_js),  v_q^T v_js = scale * d[q]
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < js; ++q) acc = fma(trow[q], d[q], acc);
+      trow[js] = (lane == js) ? tau : (lane < js ? -tau * scale * acc : 0.0);
+    }
+    if (js + 1 < kNB) {
+#pragma unroll
+      for (int c = js + 2; c < kNB; ++c)
+#pragma unroll
+        for (int q = 0; q < RQ; ++q) x[q][c] = fma(-f[c], x[q][js], x[q][c]);
+    }
+#pragma unroll
+    for (int q = 0; q < RQ; ++q) x[q][js] *= scale;
+    scale_prev = scale;
+  }
+#pragma unroll
+  for (int q = 0; q < RQ; ++q) {
+    const int rl = lane + 32 * q;
+    if (rl < brows) {
+      double* rp = Bs + rl * lds + j0;
+#pragma unroll
+      for (int c = 0; c < kNB; c += 2) *reinterpret_cast<double2*>(rp + (c ^ sw)) = make_double2(x[q][c], x[q][c + 1]);
+    }
+  }
+  if (lane < kNB) {
+    double* Rcol = R + (int64_t)j0 * npad + j0 + lane;
 #pragma unroll
     for (int jj = 0; jj < kNB; ++jj)
       if (jj <= lane) Rcol[(int64_t)jj * npad] = rmine[jj];
@@ -224,34 +404,31 @@ __device__ __forceinline__ void stage_block(double* __restrict__ dst, int lds, c
   }
 }
 
-// Stage the 8 R rows j0 .. j0+7 (columns [j0, npad)) into shared memory (stride ldr), by `nthr` threads
-// starting at thread index t0 (cp.async 16-byte copies; npad is a multiple of 8).
-__device__ __forceinline__ void stage_rrows(double* __restrict__ dst, int ldr, const double* __restrict__ R, int npad,
-                                            int j0, int t, int nthr) {
-  const int pairs = (npad - j0) >> 1;
-  for (int idx = t; idx < kNB * pairs; idx += nthr) {
-    const int r = idx / pairs, c = j0 + 2 * (idx - r * pairs);
-    cp_async16(dst + r * ldr + c, R + (int64_t)(j0 + r) * npad + c);
-  }
+// Stage the 8x8 diagonal block R(j0:j0+8, j0:j0+8) into shared memory (one warp, cp.async).
+__device__ __forceinline__ void stage_rdiag(double* __restrict__ dst, const double* __restrict__ R, int npad, int j0,
+                                            int lane) {
+  const int r = lane >> 2, c = 2 * (lane & 3);
+  cp_async16(dst + r * kNB + c, R + (int64_t)(j0 + r) * npad + j0 + c);
 }
 
 // Apply panel (j0)'s block reflector  Q^T = I - V T^T V^T  to column blocks cbs[0..G) of [R; B]:
 //   W = R_p(:, cb) + V^T B(:, cb);  W' = T^T W;  R_p(:, cb) -= W';  B(:, cb) -= V W'.
-// One warp, no CTA barrier.  R_p comes from the staged rows Rp (stride ldr); R is updated in global.
+// One warp, no CTA barrier.  The R_p tiles are read from global memory (L2-resident R slot) at the start
+// so their latency hides behind the k-loop; R is updated in global memory.
 template <int G>
 __device__ __forceinline__ void update_cbs(double* __restrict__ Bs, int lds, int brows, int j0,
-                                           const double* __restrict__ Rp, int ldr, double* __restrict__ R, int npad,
-                                           const double* __restrict__ Tm, double* __restrict__ Wsc, const int (&cbs)[G],
-                                           int lane, int tq_p) {
+                                           double* __restrict__ R, int npad, const double* __restrict__ Tm,
+                                           double* __restrict__ Wsc, const int (&cbs)[G], int lane, int tq_p) {
   const int frag_col = (lane >> 2) ^ ((lane & 2) << 1);  // slab fragment: row i + l%4, col l/4
   const int vsw = ((lane >> 2) & 2) << 1;                // V / C-tile rows 8rb + l/4
-  double acc0[G][2], acc1[G][2];
+  double acc0[G][2], acc1[G][2], rinit[G][2];
 #pragma unroll
   for (int gg = 0; gg < G; ++gg) {
-    const double* rp = Rp + (lane >> 2) * ldr + 8 * cbs[gg] + 2 * (lane & 3);
-    acc0[gg][0] = rp[0];
-    acc0[gg][1] = rp[1];
-    acc1[gg][0] = acc1[gg][1] = 0.0;
+    const double2 rv = *reinterpret_cast<const double2*>(R + (int64_t)(j0 + (lane >> 2)) * npad + 8 * cbs[gg] +
+                                                         2 * (lane & 3));
+    rinit[gg][0] = rv.x;
+    rinit[gg][1] = rv.y;
+    acc0[gg][0] = acc0[gg][1] = acc1[gg][0] = acc1[gg][1] = 0.0;
   }
   TQ_TRACE(20);
   // W = R_p + V^T B: K = brows in steps of 4 rows, two independent accumulator chains
@@ -272,17 +449,15 @@ __device__ __forceinline__ void update_cbs(double* __restrict__ Bs, int lds, int
   double wb[G][2];
 #pragma unroll
   for (int gg = 0; gg < G; ++gg) {
-    Wsc[(lane >> 2) * 8 + 2 * (lane & 3)] = acc0[gg][0] + acc1[gg][0];
-    Wsc[(lane >> 2) * 8 + 2 * (lane & 3) + 1] = acc0[gg][1] + acc1[gg][1];
+    Wsc[(lane >> 2) * 8 + 2 * (lane & 3)] = (acc0[gg][0] + acc1[gg][0]) + rinit[gg][0];
+    Wsc[(lane >> 2) * 8 + 2 * (lane & 3) + 1] = (acc0[gg][1] + acc1[gg][1]) + rinit[gg][1];
     __syncwarp();
     double w0 = 0.0, w1 = 0.0;
 #pragma unroll
     for (int k0 = 0; k0 < 8; k0 += 4)
       dmma(w0, w1, Tm[(k0 + (lane & 3)) * kNB + (lane >> 2)], Wsc[(k0 + (lane & 3)) * 8 + (lane >> 2)]);
-    const double* rps = Rp + (lane >> 2) * ldr + 8 * cbs[gg] + 2 * (lane & 3);
     double* rp = R + (int64_t)(j0 + (lane >> 2)) * npad + 8 * cbs[gg] + 2 * (lane & 3);
-    rp[0] = rps[0] - w0;
-    rp[1] = rps[1] - w1;
+    *reinterpret_cast<double2*>(rp) = make_double2(rinit[gg][0] - w0, rinit[gg][1] - w1);
     __syncwarp();
     Wsc[(lane >> 2) * 8 + 2 * (lane & 3)] = w0;
     Wsc[(lane >> 2) * 8 + 2 * (lane & 3) + 1] = w1;
@@ -325,16 +500,92 @@ __device__ __forceinline__ void update_cbs(double* __restrict__ Bs, int lds, int
 }
 
 
+// Single-warp lookahead (helper warp): panel (j0)'s block reflector applied to ONE column block cb, with
+// 4 independent DMMA accumulator chains in W = R_p + V^T B and 4 independent C tiles per iteration in
+// B -= V W' (brows % 16 == 0; the 4-tile loop handles the remainder in pairs).
+__device__ __forceinline__ void lookahead_single(double* __restrict__ Bs, int lds, int brows, int j0,
+                                                 double* __restrict__ R, int npad, const double* __restrict__ Tm,
+                                                 double* __restrict__ Wsc, int cb, int lane) {
+  const int frag_col = (lane >> 2) ^ ((lane & 2) << 1);
+  const int vsw = ((lane >> 2) & 2) << 1;
+  double* rtile = R + (int64_t)(j0 + (lane >> 2)) * npad + 8 * cb + 2 * (lane & 3);
+  const double2 rinit = *reinterpret_cast<const double2*>(rtile);
+  double c[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+  const double* slab = Bs + (lane & 3) * lds + frag_col;
+  int i = 0;
+#pragma unroll 1
+  for (; i + 16 <= brows; i += 16) {
+    double a[4], b[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double* r = slab + (i + 4 * u) * lds;
+      a[u] = r[j0];
+      b[u] = r[8 * cb];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) dmma(c[u][0], c[u][1], a[u], b[u]);
+  }
+  for (; i < brows; i += 4) {  // tail (not taken when brows % 16 == 0)
+    const double* r = slab + i * lds;
+    dmma(c[0][0], c[0][1], r[j0], r[8 * cb]);
+  }
+  Wsc[(lane >> 2) * 8 + 2 * (lane & 3)] = ((c[0][0] + c[1][0]) + (c[2][0] + c[3][0])) + rinit.x;
+  Wsc[(lane >> 2) * 8 + 2 * (lane & 3) + 1] = ((c[0][1] + c[1][1]) + (c[2][1] + c[3][1])) + rinit.y;
+  __syncwarp();
+  double w0 = 0.0, w1 = 0.0;
+#pragma unroll
+  for (int k0 = 0; k0 < 8; k0 += 4)
+    dmma(w0, w1, Tm[(k0 + (lane & 3)) * kNB + (lane >> 2)], Wsc[(k0 + (lane & 3)) * 8 + (lane >> 2)]);
+  *reinterpret_cast<double2*>(rtile) = make_double2(rinit.x - w0, rinit.y - w1);
+  __syncwarp();
+  Wsc[(lane >> 2) * 8 + 2 * (lane & 3)] = w0;
+  Wsc[(lane >> 2) * 8 + 2 * (lane & 3) + 1] = w1;
+  __syncwarp();
+  const double wb0 = -Wsc[(lane & 3) * 8 + (lane >> 2)];
+  const double wb1 = -Wsc[(4 + (lane & 3)) * 8 + (lane >> 2)];
+  __syncwarp();
+  const int nrb = brows / 8;
+  int rb = 0;
+#pragma unroll 1
+  for (; rb + 4 <= nrb; rb += 4) {
+    double* rows[4];
+    double2 cv[4];
+    double va[4], vb[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      rows[u] = Bs + (8 * (rb + u) + (lane >> 2)) * lds;
+      va[u] = rows[u][j0 + ((lane & 3) ^ vsw)];
+      vb[u] = rows[u][j0 + ((4 + (lane & 3)) ^ vsw)];
+      cv[u] = *reinterpret_cast<const double2*>(rows[u] + 8 * cb + ((2 * (lane & 3)) ^ vsw));
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) dmma(cv[u].x, cv[u].y, va[u], wb0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) dmma(cv[u].x, cv[u].y, vb[u], wb1);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) *reinterpret_cast<double2*>(rows[u] + 8 * cb + ((2 * (lane & 3)) ^ vsw)) = cv[u];
+  }
+  for (; rb < nrb; ++rb) {
+    double* row = Bs + (8 * rb + (lane >> 2)) * lds;
+    double2 cv = *reinterpret_cast<const double2*>(row + 8 * cb + ((2 * (lane & 3)) ^ vsw));
+    dmma(cv.x, cv.y, row[j0 + ((lane & 3) ^ vsw)], wb0);
+    dmma(cv.x, cv.y, row[j0 + ((4 + (lane & 3)) ^ vsw)], wb1);
+    *reinterpret_cast<double2*>(row + 8 * cb + ((2 * (lane & 3)) ^ vsw)) = cv;
+  }
+}
+
 // Cooperative lookahead: the 6 GEMM warps apply panel (j0)'s reflector to the single column block cb
 // (the next panel's columns).  GEMM1 is split over rows (k-step i/4 = gi mod 6) into 6 partial W tiles
 // summed in fixed order by GEMM warp 0, which also forms W' = T^T W and updates R; then each warp
 // updates its row blocks (rb = gi mod 6).  Two barriers among the GEMM warps only.
 __device__ __forceinline__ void lookahead_cb(double* __restrict__ Bs, int lds, int brows, int j0,
-                                             const double* __restrict__ Rp, int ldr, double* __restrict__ R, int npad,
-                                             const double* __restrict__ Tm, double* __restrict__ Wpart, int cb,
-                                             int gi, int lane) {
+                                             double* __restrict__ R, int npad, const double* __restrict__ Tm,
+                                             double* __restrict__ Wpart, int cb, int gi, int lane) {
   const int frag_col = (lane >> 2) ^ ((lane & 2) << 1);
   const int vsw = ((lane >> 2) & 2) << 1;
+  double* rtile = R + (int64_t)(j0 + (lane >> 2)) * npad + 8 * cb + 2 * (lane & 3);
+  double2 rinit = make_double2(0.0, 0.0);
+  if (gi == 0) rinit = *reinterpret_cast<const double2*>(rtile);  // early: latency hidden by the k-loop
   double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
   const double* slab = Bs + (lane & 3) * lds + frag_col;
   int it = 0;
@@ -349,8 +600,7 @@ __device__ __forceinline__ void lookahead_cb(double* __restrict__ Bs, int lds, i
   named_sync(kBarGemm, 32 * kGemmWarps);
   double* Wsh = Wpart + 6 * 64;
   if (gi == 0) {
-    const double* rps = Rp + (lane >> 2) * ldr + 8 * cb + 2 * (lane & 3);
-    double w0 = rps[0], w1 = rps[1];
+    double w0 = rinit.x, w1 = rinit.y;
 #pragma unroll
     for (int g = 0; g < kGemmWarps; ++g) {
       w0 += Wpart[g * 64 + ci];
@@ -364,9 +614,7 @@ __device__ __forceinline__ void lookahead_cb(double* __restrict__ Bs, int lds, i
 #pragma unroll
     for (int k0 = 0; k0 < 8; k0 += 4)
       dmma(v0, v1, Tm[(k0 + (lane & 3)) * kNB + (lane >> 2)], Wsh[(k0 + (lane & 3)) * 8 + (lane >> 2)]);
-    double* rp = R + (int64_t)(j0 + (lane >> 2)) * npad + 8 * cb + 2 * (lane & 3);
-    rp[0] = rps[0] - v0;
-    rp[1] = rps[1] - v1;
+    *reinterpret_cast<double2*>(rtile) = make_double2(rinit.x - v0, rinit.y - v1);
     __syncwarp();
     Wsh[ci] = v0;  // W'
     Wsh[ci + 1] = v1;
@@ -404,14 +652,13 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int npad = g.npad, lds = g.lds, brows = g.brows;
   double* Bs = smem;
-  double* Rp = smem + L::rp(g);
+  double* Rdg = smem + L::rd(g);
   double* Tm = smem + L::tm(g);
   double* red = smem + L::red(g);
   double* Wsc = smem + L::wsc(g) + warp * kNB * 8;
   double* Wpart = smem + L::wpart(g);
   double* xch = smem + L::xch(g);
   const int npanels = npad / kNB, ncb = npad / 8;
-  const int ldr = lds;
   const bool vec16 = ((ldsrc & 1) == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
 
   if (init_zero) {
@@ -424,7 +671,7 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
     const int p0 = triangular ? (int)min64(r0 / kNB, npanels) : 0;
     __syncthreads();  // previous block fully consumed; R (init or previous block) visible
     stage_block(Bs, lds, src + r0 * ldsrc, ldsrc, cnt, ncols, brows, npad, vec16);
-    if (p0 < npanels) stage_rrows(Rp + (p0 & 1) * kNB * ldr, ldr, R, npad, p0 * kNB, tid, kTqThreads);
+    if (p0 < npanels && warp == 0) stage_rdiag(Rdg + (p0 & 1) * kNB * kNB, R, npad, p0 * kNB, lane);
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
@@ -447,42 +694,57 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
     for (int p = p0; p < npanels; ++p) {
       const int j0 = p * kNB;
       const int buf = p & 1;
-      const double* Rpc = Rp + buf * kNB * ldr;
+      const double* Rdc = Rdg + buf * kNB * kNB;
       const double* Tmc = Tm + buf * kNB * kNB;
       const bool more = p + 1 < npanels;
       const int tq_p = (r0 == 0 && p < 64) ? p : -1;
       if (warp == 0 || (NPW == 2 && warp == 4)) {
         if (p > p0) named_sync(kBarColsReady, kTqThreads);
+        TQ_RESOLVE(Rdg);
         TQ_TRACE(1);
-        panel_factor<RQ, NPW>(Bs, lds, brows, j0, R, npad, Rpc, ldr, Tm + buf * kNB * kNB, red, xch, warp >> 2,
-                              lane, tq_p);
+        if (NPW == 1 && kLazyPanel)
+          panel_factor_lazy<RQ>(Bs, lds, brows, j0, R, npad, Rdc, Tm + buf * kNB * kNB, red, lane, tq_p);
+        else
+          panel_factor<RQ, NPW>(Bs, lds, brows, j0, R, npad, Rdc, Tm + buf * kNB * kNB, red, xch, warp >> 2, lane,
+                                tq_p);
         TQ_TRACE(2);
         named_arrive(kBarPanelDone, kTqThreads);
-      } else if (warp == 4) {  // NPW == 1: helper on SMSP 0 (no DMMA): stages the R rows of panel p+1
+      } else if (warp == 4) {
+        // NPW == 1: helper on SMSP 0.  While the panel warp waits for ColsReady it is idle, so the helper
+        // does the lookahead alone (update of the next panel's column block with panel p) plus the R diag
+        // staging; it starts the moment the panel is published instead of after the GEMM warps' trailing
+        // work, and its DMMAs never overlap the panel's FP64 chain on this SMSP.
         named_sync(kBarPanelDone, kTqThreads);
+        TQ_RESOLVE(Rdg);
         if (more) {
-          stage_rrows(Rp + (buf ^ 1) * kNB * ldr, ldr, R, npad, j0 + kNB, lane, 32);
+          TQ_TRACE(3);
+          stage_rdiag(Rdg + (buf ^ 1) * kNB * kNB, R, npad, j0 + kNB, lane);
           cp_async_commit();
+          if (kHelperLookahead) lookahead_single(Bs, lds, brows, j0, R, npad, Tmc, Wsc, p + 1, lane);
           cp_async_wait<0>();
           __syncwarp();
+          TQ_TRACE(4);
           named_arrive(kBarColsReady, kTqThreads);
         }
       } else {
         const int gi = gemm_index(warp);
         named_sync(kBarPanelDone, kTqThreads);
+        TQ_RESOLVE(Rdg);
         if (more) {
-          TQ_TRACE(3);
-          const bool stager = NPW == 2 && gi == 0;  // with two panel warps, GEMM warp 0 stages R rows
-          if (stager) {
-            stage_rrows(Rp + (buf ^ 1) * kNB * ldr, ldr, R, npad, j0 + kNB, lane, 32);
-            cp_async_commit();
+          if (NPW == 2 || !kHelperLookahead) {
+            TQ_TRACE(3);
+            const bool stager = NPW == 2 && gi == 0;  // with two panel warps, GEMM warp 0 stages the R diag block
+            if (stager) {
+              stage_rdiag(Rdg + (buf ^ 1) * kNB * kNB, R, npad, j0 + kNB, lane);
+              cp_async_commit();
+            }
+            lookahead_cb(Bs, lds, brows, j0, R, npad, Tmc, Wpart, p + 1, gi, lane);
+            if (stager) {
+              cp_async_wait<0>();
+              __syncwarp();
+            }
+            TQ_TRACE(4);
           }
-          lookahead_cb(Bs, lds, brows, j0, Rpc, ldr, R, npad, Tmc, Wpart, p + 1, gi, lane);
-          if (stager) {
-            cp_async_wait<0>();
-            __syncwarp();
-          }
-          TQ_TRACE(4);
           named_arrive(kBarColsReady, kTqThreads);
         }
         // trailing column blocks p+2 .. ncb-1, round-robin over the GEMM warps in groups of G
@@ -495,11 +757,11 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
             if (cbs[gg] < ncb) ++cnt_g;
           }
           if (cnt_g == G) {
-            update_cbs<G>(Bs, lds, brows, j0, Rpc, ldr, R, npad, Tmc, Wsc, cbs, lane, tq_p);
+            update_cbs<G>(Bs, lds, brows, j0, R, npad, Tmc, Wsc, cbs, lane, tq_p);
           } else {
             for (int gg = 0; gg < cnt_g; ++gg) {
               const int one[1] = {cbs[gg]};
-              update_cbs<1>(Bs, lds, brows, j0, Rpc, ldr, R, npad, Tmc, Wsc, one, lane, tq_p);
+              update_cbs<1>(Bs, lds, brows, j0, R, npad, Tmc, Wsc, one, lane, tq_p);
             }
           }
         }

@@ -27,11 +27,15 @@ upd = np.nanmean([[d(0, p, 30 + j, 10 + j + 1) if j < 7 else d(0, p, 37, 2) for 
 print(f"panel warp: panel {np.nanmean(panel):.0f} clk, wait for ColsReady {np.nanmean(wait):.0f}, first col start {np.nanmean([d(0,p,1,10) for p in range(P)]):.0f}")
 print("  per column reduce:", red.astype(int).tolist())
 print("  per column update:", upd.astype(int).tolist())
-for w in (1, 2, 3, 5, 6, 7):
+for w in (1, 2, 3, 4, 5, 6, 7):
     la = np.nanmean([d(w, p, 3, 4) for p in range(P)])
     g1 = np.nanmean([d(w, p, 20, 21) for p in range(P)])
     g2 = np.nanmean([d(w, p, 21, 22) for p in range(P)])
     g3 = np.nanmean([d(w, p, 22, 23) for p in range(P)])
     print(f"gemm warp {w}: lookahead {la:.0f}, last group: W {g1:.0f}, T/R {g2:.0f}, B-=VW {g3:.0f}")
+lw = 4 if np.nansum(t[4, :, 3]) > 0 else 1
+la_start = [t[lw, p, 3] - t[0, p, 2] for p in range(P - 1)]
+la_to_panel = [t[0, p + 1, 1] - t[lw, p, 4] for p in range(P - 1)]
+print(f"panel done -> lookahead start {np.nanmean(la_start):.0f}, lookahead end -> next panel start {np.nanmean(la_to_panel):.0f}, panel start -> col0 {np.nanmean([d(0,p,1,10) for p in range(P)]):.0f}, col7 end -> panel done {np.nanmean([d(0,p,37,2) for p in range(P)]):.0f}")
 tot = t[0, P - 1, 2] - t[0, 0, 1]
 print(f"block span (panel 0 start -> last panel done): {tot:.0f} clk = {tot / P:.0f} per panel")
