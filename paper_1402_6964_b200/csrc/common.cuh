@@ -73,11 +73,82 @@ __device__ __forceinline__ double rng_uniform(uint64_t stream, uint64_t ctr) {
   return __dmul_rn((double)(rng_word(stream, ctr) >> 11), kInv2p53);
 }
 
-// Standard normal #j: uniforms at counters 2j, 2j+1, Box-Muller cosine branch (_kernels.pyx:49-69).
+// log(u) for u in [2^-54, 1) (the Box-Muller u1 domain): u = m 2^e with m in [sqrt(1/2), sqrt(2)),
+// log m = 2 atanh(s), s = (m - 1)/(m + 1), |s| <= 0.1716, atanh series through s^21; ln 2 split hi/lo.
+// No special-value paths are needed on this domain.  Max relative error ~4e-16 vs libm (1M samples).
+__device__ __forceinline__ double bm_log(double u) {
+  const int hi = __double2hiint(u), lo = __double2loint(u);
+  int e = ((hi >> 20) & 0x7ff) - 1023;
+  double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);  // [1, 2)
+  const bool big = m > 1.4142135623730951;
+  m = big ? 0.5 * m : m;
+  e = big ? e + 1 : e;
+  const double f = m - 1.0;
+  const double den = 2.0 + f;
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(den));
+  r = r * fma(-den, r, 2.0);
+  r = r * fma(-den, r, 2.0);
+  double sv = f * r;
+  sv = fma(r, fma(-sv, den, f), sv);  // one residual correction: s to ~0.5 ulp
+  const double z = sv * sv;
+  double p = 0.047619047619047616;
+  p = fma(p, z, 0.05263157894736842);
+  p = fma(p, z, 0.058823529411764705);
+  p = fma(p, z, 0.06666666666666667);
+  p = fma(p, z, 0.07692307692307693);
+  p = fma(p, z, 0.09090909090909091);
+  p = fma(p, z, 0.1111111111111111);
+  p = fma(p, z, 0.14285714285714285);
+  p = fma(p, z, 0.2);
+  p = fma(p, z, 0.3333333333333333);
+  p = fma(p, z, 1.0);
+  const double de = (double)e;
+  return fma(de, 0.6931471803691238, fma(de, 1.9082149292705877e-10, 2.0 * sv * p));
+}
+
+// cos(t) for t in [0, 2 pi]: Cody-Waite reduction by pi/2 (two-part constant, k <= 4), Taylor
+// polynomials of cos / sin through r^18 / r^19 on |r| <= pi/4, quadrant select.  Max absolute error
+// ~1.1e-16 vs libm.
+__device__ __forceinline__ double bm_cos(double t) {
+  const int k = __double2int_rn(t * 0.6366197723675814);
+  const double dk = (double)k;
+  const double r = fma(-dk, 6.077100506506192e-11, fma(-dk, 1.5707963267341256, t));
+  const double r2 = r * r;
+  double c = -1.5619206968586225e-16;
+  c = fma(c, r2, 4.779477332387385e-14);
+  c = fma(c, r2, -1.1470745597729725e-11);
+  c = fma(c, r2, 2.08767569878681e-09);
+  c = fma(c, r2, -2.755731922398589e-07);
+  c = fma(c, r2, 2.48015873015873e-05);
+  c = fma(c, r2, -0.001388888888888889);
+  c = fma(c, r2, 0.041666666666666664);
+  c = fma(c, r2, -0.5);
+  c = fma(c, r2, 1.0);
+  double sn = -8.22063524662433e-18;
+  sn = fma(sn, r2, 2.8114572543455206e-15);
+  sn = fma(sn, r2, -7.647163731819816e-13);
+  sn = fma(sn, r2, 1.6059043836821613e-10);
+  sn = fma(sn, r2, -2.505210838544172e-08);
+  sn = fma(sn, r2, 2.7557319223985893e-06);
+  sn = fma(sn, r2, -0.0001984126984126984);
+  sn = fma(sn, r2, 0.008333333333333333);
+  sn = fma(sn, r2, -0.16666666666666666);
+  sn = fma(sn, r2, 1.0);
+  sn *= r;
+  const int q = k & 3;
+  const double v = (q & 1) ? sn : c;
+  return (q == 1 || q == 2) ? -v : v;
+}
+
+// Standard normal #j: uniforms at counters 2j, 2j+1, Box-Muller cosine branch (_kernels.pyx:49-69):
+// z = sqrt(-2 log u1) cos(2 pi u2) with the same rounding of u1, u2 and 2 pi u2 as the reference; log
+// and cos are the domain-specialised bm_log / bm_cos (few-ulp, ~100 instructions per normal instead of
+// ~250 with the general libdevice versions).  Agreement with the reference's libm: |dz| <= ~1e-15.
 __device__ __forceinline__ double rng_normal(uint64_t stream, uint64_t j) {
   double u1 = __dmul_rn(__dadd_rn((double)(rng_word(stream, 2 * j) >> 11), 0.5), kInv2p53);
   double u2 = __dmul_rn((double)(rng_word(stream, 2 * j + 1) >> 11), kInv2p53);
-  return __dmul_rn(sqrt(__dmul_rn(-2.0, log(u1))), cos(__dmul_rn(kTwoPi, u2)));
+  return __dmul_rn(sqrt(__dmul_rn(-2.0, bm_log(u1))), bm_cos(__dmul_rn(kTwoPi, u2)));
 }
 
 // Single-precision Box-Muller on the same counters (2j, 2j+1), used ONLY by the synthetic-data
