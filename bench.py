@@ -1,7 +1,7 @@
 """Benchmark of the single-pass reduction (BASELINE.json metric: 1-pass TSQR/Gram
 GB/s of X and % of roofline), one JSON line on rank 0.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--m M]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--rows M]
   python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
   python bench.py --impl reference            # the reference's CPU path (oracle port) on host cores
 
@@ -61,7 +61,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="C2")
-    p.add_argument("--m", type=int, default=None, help="override total rows")
+    p.add_argument("--rows", type=int, default=None, help="override total rows m")
     p.add_argument("--k", type=int, default=400, help="sketch rows for the GX pass")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
@@ -230,8 +230,8 @@ def main():
     lib = _native.load()
 
     spec = synthetic.config(args.config)
-    if args.m:
-        spec = synthetic.config(args.config, m=args.m)
+    if args.rows:
+        spec = synthetic.config(args.config, m=args.rows)
     m, n = spec.m, spec.n
     lo, hi = sharded.shard_range(m, world, rank)
     x = torch.empty((hi - lo, n), dtype=torch.float64, device=devc)

@@ -8,9 +8,9 @@ nvidia-smi --query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_rea
 CPID=$!
 timeout 900 python bench.py > gpurun_out/bench_full.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench_full.log
 kill $CPID
-python bench.py --m 4194304 --steps 2 --warmup 1 --no-cpu --no-e2e > gpurun_out/bench_ncu_plain.log 2>&1 && \
+python bench.py --rows 4194304 --steps 2 --warmup 1 --no-cpu --no-e2e > gpurun_out/bench_ncu_plain.log 2>&1 && \
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
-  python bench.py --m 4194304 --steps 2 --warmup 1 --no-cpu --no-e2e > gpurun_out/ncu_launches.log 2>&1
+  python bench.py --rows 4194304 --steps 2 --warmup 1 --no-cpu --no-e2e > gpurun_out/ncu_launches.log 2>&1
 python tools/run_kernel.py tsqr 2097152 200 1 > gpurun_out/plain.log 2>&1 && \
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:tsqr_leaf -c 1 -o gpurun_out/tsqr_leaf_full \
   python tools/run_kernel.py tsqr 2097152 200 1 > gpurun_out/ncu_full.log 2>&1

@@ -18,7 +18,7 @@ def launches():
         name = r[ix["Kernel Name"]].split("(")[0]
         agg[name][0] += 1; agg[name][1] += v
     tot = sum(v for _, v in agg.values())
-    lines = [f"# ncu launch list ({tag}): python bench.py --m 4194304 --steps 2 --warmup 1 --no-cpu --no-e2e",
+    lines = [f"# ncu launch list ({tag}): python bench.py --rows 4194304 --steps 2 --warmup 1 --no-cpu --no-e2e",
              "# ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised: compare SHARES)",
              f"{'kernel':60s} {'launches':>8s} {'total_ms':>10s} {'share':>7s}"]
     for name, (n, v) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
