@@ -368,7 +368,15 @@ def main():
                 off += take
 
         def e2e_step():
-            return tb.stream_pass(chunks())
+            res = tb.stream_pass(chunks())
+            if world > 1:  # same exchange as the resident path: all-gather + ordered device combine
+                part = sharded.ShardPartials(
+                    r=torch.as_tensor(res.factor.entries, device=devc),
+                    l1=torch.as_tensor(res.stats.l1, device=devc),
+                    sumsq=torch.as_tensor(res.stats.l2 ** 2, device=devc), rows=res.rows)
+                out = sharded.exchange(part, dv.combine_factors)
+                out.r.cpu()
+            return res
 
         e2e_step()
         barrier()
@@ -380,7 +388,8 @@ def main():
         e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / e_steps)
         line["e2e"] = {"value": bytes_total / (e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e_ms,
                        "h2d_bytes_per_step": bytes_local, "d2h_bytes_per_step": (n * n + 2 * n) * 8,
-                       "api": "paper_1402_6964_b200.stream_pass over host RowChunks (65536 rows each)",
+                       "api": "paper_1402_6964_b200.stream_pass over host RowChunks (65536 rows each)"
+                              + (" + NCCL all-gather + ordered device combine" if world > 1 else ""),
                        "host_pool": f"{pool_rows} pinned rows cycled (QR cost is data-independent)",
                        "steps": e_steps, "timer": "host wall clock around the API call, barrier on both sides"}
         assert res.rows == hi - lo
