@@ -197,70 +197,63 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 __host__ __device__ __forceinline__ int swz_row(int row) { return (row & 2) << 1; }
 __host__ __device__ __forceinline__ int swz_col(int row, int col) { return col ^ swz_row(row); }
 
-// Swizzled variant of stage_rows below (same contract; cols_total must be a multiple of 8).
-__device__ __forceinline__ void stage_rows_swz(double* __restrict__ dst, int lds, const double* __restrict__ src,
-                                               int64_t ldsrc, int nrows, int ncols, int rows_total,
-                                               int cols_total, bool vec16) {
+// Row-major walk over the cells {start, start + step, ...} of a grid with w columns, with one division
+// up front and a carry per step instead of a division per cell (the staging loops below issue one
+// cp.async per cell, so the index math is their cost).
+struct GridWalk {
+  int r, c, dr, dc, w;
+  __device__ __forceinline__ GridWalk(int start, int step, int w_) : w(w_) {
+    r = start / w;
+    c = start - r * w;
+    dr = step / w;
+    dc = step - dr * w;
+  }
+  __device__ __forceinline__ void next() {
+    r += dr;
+    c += dc;
+    if (c >= w) {
+      c -= w;
+      ++r;
+    }
+  }
+};
+
+// Stage rows [0, nrows) x cols [0, ncols) of a row-major global matrix into shared memory with row
+// stride lds (swizzled: column c of row r at r*lds + swz_col(r, c)); rows [nrows, rows_total) and cols
+// [ncols, cols_total) are zero-filled.  cols_total must be a multiple of 8.  All threads of the CTA
+// participate; the caller commits / waits.
+template <bool kSwz>
+__device__ __forceinline__ void stage_rows_impl(double* __restrict__ dst, int lds, const double* __restrict__ src,
+                                                int64_t ldsrc, int nrows, int ncols, int rows_total,
+                                                int cols_total, bool vec16) {
   const int tid = threadIdx.x, nth = blockDim.x;
+  auto at = [&](int r, int c) -> double* { return dst + (int64_t)r * lds + (kSwz ? swz_col(r, c) : c); };
   if (vec16) {
     const int pairs = ncols >> 1;
-    for (int idx = tid; idx < nrows * pairs; idx += nth) {
-      const int r = idx / pairs, c = (idx - r * pairs) * 2;
-      cp_async16(dst + (int64_t)r * lds + swz_col(r, c), src + r * ldsrc + c);
-    }
+    if (pairs > 0)
+      for (GridWalk it(tid, nth, pairs); it.r < nrows; it.next())
+        cp_async16(at(it.r, 2 * it.c), src + it.r * ldsrc + 2 * it.c);
     if (ncols & 1)
-      for (int r = tid; r < nrows; r += nth)
-        cp_async8(dst + (int64_t)r * lds + swz_col(r, ncols - 1), src + r * ldsrc + ncols - 1);
-  } else {
-    for (int idx = tid; idx < nrows * ncols; idx += nth) {
-      const int r = idx / ncols, c = idx - r * ncols;
-      cp_async8(dst + (int64_t)r * lds + swz_col(r, c), src + r * ldsrc + c);
-    }
+      for (int r = tid; r < nrows; r += nth) cp_async8(at(r, ncols - 1), src + r * ldsrc + ncols - 1);
+  } else if (ncols > 0) {
+    for (GridWalk it(tid, nth, ncols); it.r < nrows; it.next()) cp_async8(at(it.r, it.c), src + it.r * ldsrc + it.c);
   }
   const int pad = cols_total - ncols;
   if (pad > 0)
-    for (int idx = tid; idx < nrows * pad; idx += nth) {
-      const int r = idx / pad, c = ncols + (idx - r * pad);
-      dst[(int64_t)r * lds + swz_col(r, c)] = 0.0;
-    }
-  for (int idx = tid; idx < (rows_total - nrows) * cols_total; idx += nth) {
-    const int r = nrows + idx / cols_total, c = idx % cols_total;
-    dst[(int64_t)r * lds + c] = 0.0;
-  }
+    for (GridWalk it(tid, nth, pad); it.r < nrows; it.next()) *at(it.r, ncols + it.c) = 0.0;
+  if (rows_total > nrows && cols_total > 0)
+    for (GridWalk it(tid, nth, cols_total); it.r < rows_total - nrows; it.next()) *at(nrows + it.r, it.c) = 0.0;
 }
 
-// Stage rows [0, nrows) x cols [0, ncols) of a row-major global matrix into shared memory with
-// row stride lds; rows [nrows, rows_total) and cols [ncols, cols_total) are zero-filled.
-// All threads of the CTA participate.  Caller commits / waits.
+__device__ __forceinline__ void stage_rows_swz(double* __restrict__ dst, int lds, const double* __restrict__ src,
+                                               int64_t ldsrc, int nrows, int ncols, int rows_total,
+                                               int cols_total, bool vec16) {
+  stage_rows_impl<true>(dst, lds, src, ldsrc, nrows, ncols, rows_total, cols_total, vec16);
+}
 __device__ __forceinline__ void stage_rows(double* __restrict__ dst, int lds, const double* __restrict__ src,
                                            int64_t ldsrc, int nrows, int ncols, int rows_total,
                                            int cols_total, bool vec16) {
-  const int tid = threadIdx.x, nth = blockDim.x;
-  if (vec16) {
-    const int pairs = ncols >> 1;
-    for (int idx = tid; idx < nrows * pairs; idx += nth) {
-      int r = idx / pairs, c = (idx - r * pairs) * 2;
-      cp_async16(dst + (int64_t)r * lds + c, src + r * ldsrc + c);
-    }
-    if (ncols & 1)
-      for (int r = tid; r < nrows; r += nth) cp_async8(dst + (int64_t)r * lds + ncols - 1, src + r * ldsrc + ncols - 1);
-  } else {
-    for (int idx = tid; idx < nrows * ncols; idx += nth) {
-      int r = idx / ncols, c = idx - r * ncols;
-      cp_async8(dst + (int64_t)r * lds + c, src + r * ldsrc + c);
-    }
-  }
-  if (ncols < cols_total) {
-    const int pad = cols_total - ncols;
-    for (int idx = tid; idx < nrows * pad; idx += nth) {
-      int r = idx / pad, c = ncols + (idx - r * pad);
-      dst[(int64_t)r * lds + c] = 0.0;
-    }
-  }
-  for (int idx = tid; idx < (rows_total - nrows) * cols_total; idx += nth) {
-    int r = nrows + idx / cols_total, c = idx % cols_total;
-    dst[(int64_t)r * lds + c] = 0.0;
-  }
+  stage_rows_impl<false>(dst, lds, src, ldsrc, nrows, ncols, rows_total, cols_total, vec16);
 }
 
 }  // namespace tsnmf

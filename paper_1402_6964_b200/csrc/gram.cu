@@ -14,9 +14,12 @@
 
 namespace tsnmf {
 
-constexpr int kGrThreads = 256;
-constexpr int kGrWarps = kGrThreads / 32;
-constexpr int kGrSpw = 12;   // super-tiles per warp (96 accumulator doubles)
+#ifndef TSNMF_GRAM_WARPS
+#define TSNMF_GRAM_WARPS 8
+#endif
+constexpr int kGrWarps = TSNMF_GRAM_WARPS;   // 2 per SMSP; 12 / 16 measured slower (fewer tiles per warp, spills)
+constexpr int kGrThreads = 32 * kGrWarps;
+constexpr int kGrSpw = 96 / kGrWarps;        // super-tiles per warp (96 per CTA = one group at n <= 208)
 constexpr int kGrBrMax = 64; // rows per stage (halved until the double buffer fits)
 
 struct GrGeom {
@@ -99,9 +102,18 @@ __global__ void __launch_bounds__(kGrThreads, 1)
       for (int h = 0; h < 2; ++h) {
         const int col = tid + h * kGrThreads;
         if (col < g.n) {
-          double a = l1a[h];
-          for (int i = 0; i < br; ++i) a += fabs(xs[i * lds + swz_col(i, col)]);
-          l1a[h] = a;
+          // 4 independent chains so the adds pipeline (br % 4 == 0; rows 4j+2, 4j+3 are XOR-4 swizzled);
+          // the summation order is fixed, so the result stays deterministic
+          const double* p = xs + col;
+          const double* q = xs + (col ^ 4);
+          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+          for (int i = 0; i < br; i += 4) {
+            a0 += fabs(p[(i + 0) * lds]);
+            a1 += fabs(p[(i + 1) * lds]);
+            a2 += fabs(q[(i + 2) * lds]);
+            a3 += fabs(q[(i + 3) * lds]);
+          }
+          l1a[h] += (a0 + a1) + (a2 + a3);
         }
       }
     }
@@ -180,7 +192,7 @@ GrGeom gr_geom(int64_t m, int n, int sms) {
   g.lds = smem_stride(g.npad);
   g.ns = g.npad / 16;
   g.nst = g.ns * (g.ns + 1) / 2;
-  g.ks = 8;  // k-slices: as many as keep every warp busy
+  g.ks = kGrWarps;  // k-slices: as many as keep every warp busy
   while (g.ks > 1 && (kGrWarps / g.ks) * kGrSpw < g.nst) g.ks /= 2;
   g.spc = (kGrWarps / g.ks) * kGrSpw;
   g.groups = (int)ceil_div(g.nst, g.spc);
