@@ -177,6 +177,8 @@ __host__ __device__ __forceinline__ int smem_stride(int cols) {
   return s;
 }
 
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
 // cp.async helpers (LDGSTS): global -> shared without staging through registers.
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);

@@ -20,7 +20,7 @@ namespace tsnmf {
 constexpr int kGrWarps = TSNMF_GRAM_WARPS;   // 2 per SMSP; 12 / 16 measured slower (fewer tiles per warp, spills)
 constexpr int kGrThreads = 32 * kGrWarps;
 constexpr int kGrSpw = 96 / kGrWarps;        // super-tiles per warp (96 per CTA = one group at n <= 208)
-constexpr int kGrBrMax = 64; // rows per stage (halved until the double buffer fits)
+constexpr int kGrBrMax = 128;  // rows per stage (halved until the double buffer fits)
 
 struct GrGeom {
   int n, npad;  // npad = round_up(n, 16)

@@ -373,35 +373,11 @@ __device__ __forceinline__ void panel_factor_lazy(double* __restrict__ Bs, int l
 }
 
 // Stage rows into the swizzled block layout (cp.async); zero-fill padding rows / columns.
+// swz(r) == swz_row(r), so this is the shared division-free swizzled staging loop.
 __device__ __forceinline__ void stage_block(double* __restrict__ dst, int lds, const double* __restrict__ src,
                                             int64_t ldsrc, int nrows, int ncols, int rows_total, int cols_total,
                                             bool vec16) {
-  const int tid = threadIdx.x;
-  if (vec16) {
-    const int pairs = ncols >> 1;
-    for (int idx = tid; idx < nrows * pairs; idx += kTqThreads) {
-      const int r = idx / pairs, c = (idx - r * pairs) * 2;
-      cp_async16(dst + r * lds + (c ^ swz(r)), src + r * ldsrc + c);
-    }
-    if (ncols & 1)
-      for (int r = tid; r < nrows; r += kTqThreads)
-        cp_async8(dst + r * lds + ((ncols - 1) ^ swz(r)), src + r * ldsrc + ncols - 1);
-  } else {
-    for (int idx = tid; idx < nrows * ncols; idx += kTqThreads) {
-      const int r = idx / ncols, c = idx - r * ncols;
-      cp_async8(dst + r * lds + (c ^ swz(r)), src + r * ldsrc + c);
-    }
-  }
-  const int pad = cols_total - ncols;
-  if (pad > 0)
-    for (int idx = tid; idx < nrows * pad; idx += kTqThreads) {
-      const int r = idx / pad, c = ncols + (idx - r * pad);
-      dst[r * lds + (c ^ swz(r))] = 0.0;
-    }
-  for (int idx = tid; idx < (rows_total - nrows) * cols_total; idx += kTqThreads) {
-    const int r = nrows + idx / cols_total, c = idx % cols_total;
-    dst[r * lds + c] = 0.0;
-  }
+  stage_rows_swz(dst, lds, src, ldsrc, nrows, ncols, rows_total, cols_total, vec16);
 }
 
 // Stage the 8x8 diagonal block R(j0:j0+8, j0:j0+8) into shared memory (one warp, cp.async).
