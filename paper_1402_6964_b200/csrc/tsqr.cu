@@ -857,11 +857,13 @@ bool tq_choose(int n, int minb, TqChoice* out) {
 }
 
 bool tq_config(int n, TqChoice* out) {
-  // Occupancy: 1 CTA / SM with the largest block that fits (rows in flight per panel chain bound the
-  // throughput); TSNMF_TSQR_CTAS=2 selects two half-size CTAs per SM for tuning.
-  int minb = 1;
+  // Occupancy: the throughput is (rows in flight) / (n x per-column panel latency) per panel chain (see
+  // DESIGN.md).  Narrow matrices (n <= 64) fit a full 128-row block in half the shared memory, so two CTAs
+  // per SM give two independent panel chains (measured +50% at n = 25 and 64); wider ones run one CTA
+  // with the largest block.  TSNMF_TSQR_CTAS=1/2 overrides for tuning.
+  int minb = n <= 64 ? 2 : 1;
   if (const char* e = getenv("TSNMF_TSQR_CTAS")) minb = atoi(e) == 2 ? 2 : 1;
-  if (minb == 2 && tq_choose(n, 2, out) && out->g.brows >= 48) return true;
+  if (minb == 2 && tq_choose(n, 2, out) && out->g.brows >= (n <= 64 ? 128 : 48)) return true;
   return tq_choose(n, 1, out);
 }
 
