@@ -19,8 +19,8 @@ namespace tsnmf {
 #endif
 constexpr int kGrWarps = TSNMF_GRAM_WARPS;   // 2 per SMSP; 12 / 16 measured slower (fewer tiles per warp, spills)
 constexpr int kGrThreads = 32 * kGrWarps;
-constexpr int kGrSpw = 96 / kGrWarps;        // super-tiles per warp (96 per CTA = one group at n <= 208)
-constexpr int kGrBrMax = 128;  // rows per stage (halved until the double buffer fits)
+constexpr int kGrSpwMax = 96 / kGrWarps;     // super-tiles per warp (96 per CTA = one group at n <= 208)
+constexpr int kGrBrMax = 256;  // rows per stage (halved until the double buffer fits)
 
 struct GrGeom {
   int n, npad;  // npad = round_up(n, 16)
@@ -28,7 +28,8 @@ struct GrGeom {
   int ns;       // super-blocks per side (npad / 16)
   int nst;      // super-tiles in the upper triangle
   int ks;       // k-slices per CTA (warps sharing a super-tile set, splitting the rows)
-  int spc;      // super-tiles per CTA (tile group) = (8 / ks) * kGrSpw
+  int spw;      // super-tiles per warp (kernel template: 1, 3, 6, 10 or 12)
+  int spc;      // super-tiles per CTA (tile group) = (8 / ks) * spw
   int groups;   // tile groups
   int br;       // rows per stage
   int64_t rows_per_split;
@@ -46,8 +47,9 @@ __host__ __device__ inline void st_coords(int idx, int ns, int* P, int* Q) {
 }
 
 // Warp w = kslice + ks * wi: k-slice `kslice` takes the 4-row k-steps i/4 = kslice (mod ks); warp index
-// wi within the slice owns a contiguous run of kGrSpw super-tiles (consecutive super-tiles mostly share
+// wi within the slice owns a contiguous run of SPW super-tiles (consecutive super-tiles mostly share
 // their row P, so the A fragments are reused).  Partials: [split][kslice][supertile][16][16].
+template <int SPW>
 __global__ void __launch_bounds__(kGrThreads, 1)
     gram_kernel(const double* __restrict__ x, int64_t m, int64_t ldx, GrGeom g, double* __restrict__ partial,
                 double* __restrict__ l1part) {
@@ -62,22 +64,25 @@ __global__ void __launch_bounds__(kGrThreads, 1)
   const bool vec16 = ((ldx & 1) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
 
   // packed super-tile coordinates: (16 P) << 16 | 16 Q; the first nvalid are real
-  int stPQ[kGrSpw];
-  const int first = group * g.spc + wi * kGrSpw;
-  const int nvalid = max(0, min(kGrSpw, g.nst - first));
+  int stPQ[SPW];
+  const int first = group * g.spc + wi * SPW;
+  const int nvalid = max(0, min(SPW, g.nst - first));
 #pragma unroll
-  for (int u = 0; u < kGrSpw; ++u) {
+  for (int u = 0; u < SPW; ++u) {
     int P = 0, Q = 0;
     if (u < nvalid) st_coords(first + u, g.ns, &P, &Q);
     stPQ[u] = (16 * P) << 16 | (16 * Q);
   }
-  double acc[kGrSpw][4][2];
+  double acc[SPW][4][2];
 #pragma unroll
-  for (int u = 0; u < kGrSpw; ++u)
+  for (int u = 0; u < SPW; ++u)
 #pragma unroll
     for (int t = 0; t < 4; ++t) acc[u][t][0] = acc[u][t][1] = 0.0;
   double l1a[2] = {0.0, 0.0};
   const bool do_l1 = (group == 0) && (l1part != nullptr);
+  // column l1: narrow matrices split each column's rows over l1_ph thread phases
+  const int l1_ph = g.npad <= kGrThreads / 2 ? kGrThreads / g.npad : 1;
+  const int l1_c = tid % g.npad, l1_r0 = tid / g.npad;
   const int frag_col = (lane >> 2) ^ ((lane & 2) << 1);  // swizzled slab fragment: row i + l%4, col l/4
 
   const int64_t nstages = ceil_div(max64(rend - rbeg, 0), br);
@@ -98,22 +103,31 @@ __global__ void __launch_bounds__(kGrThreads, 1)
     __syncthreads();
     const double* xs = smem + (s & 1) * br * lds;
     if (do_l1) {
+      if (l1_ph > 1) {
+        // narrow: thread = (row phase, column); rows i = phase (mod l1_ph)
+        if (l1_r0 < l1_ph && l1_c < g.n) {
+          double a = 0.0;
+          for (int i = l1_r0; i < br; i += l1_ph) a += fabs(xs[i * lds + swz_col(i, l1_c)]);
+          l1a[0] += a;
+        }
+      } else {
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int col = tid + h * kGrThreads;
-        if (col < g.n) {
-          // 4 independent chains so the adds pipeline (br % 4 == 0; rows 4j+2, 4j+3 are XOR-4 swizzled);
-          // the summation order is fixed, so the result stays deterministic
-          const double* p = xs + col;
-          const double* q = xs + (col ^ 4);
-          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-          for (int i = 0; i < br; i += 4) {
-            a0 += fabs(p[(i + 0) * lds]);
-            a1 += fabs(p[(i + 1) * lds]);
-            a2 += fabs(q[(i + 2) * lds]);
-            a3 += fabs(q[(i + 3) * lds]);
+        for (int h = 0; h < 2; ++h) {
+          const int col = tid + h * kGrThreads;
+          if (col < g.n) {
+            // 4 independent chains so the adds pipeline (br % 4 == 0; rows 4j+2, 4j+3 are XOR-4 swizzled);
+            // the summation order is fixed, so the result stays deterministic
+            const double* p = xs + col;
+            const double* q = xs + (col ^ 4);
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            for (int i = 0; i < br; i += 4) {
+              a0 += fabs(p[(i + 0) * lds]);
+              a1 += fabs(p[(i + 1) * lds]);
+              a2 += fabs(q[(i + 2) * lds]);
+              a3 += fabs(q[(i + 3) * lds]);
+            }
+            l1a[h] += (a0 + a1) + (a2 + a3);
           }
-          l1a[h] += (a0 + a1) + (a2 + a3);
         }
       }
     }
@@ -123,7 +137,7 @@ __global__ void __launch_bounds__(kGrThreads, 1)
     for (int i = 4 * kslice; i < br; i += 4 * ks) {
       const double* row = xs + (i + (lane & 3)) * lds + frag_col;
 #pragma unroll
-      for (int u = 0; u < kGrSpw; ++u) {
+      for (int u = 0; u < SPW; ++u) {
         const int P16 = stPQ[u] >> 16, Q16 = stPQ[u] & 0xffff;
         const double a0 = row[P16], a1 = row[P16 + 8];
         const double b0 = row[Q16], b1 = row[Q16 + 8];
@@ -136,7 +150,7 @@ __global__ void __launch_bounds__(kGrThreads, 1)
     __syncthreads();  // buffer reuse
   }
 #pragma unroll
-  for (int u = 0; u < kGrSpw; ++u) {
+  for (int u = 0; u < SPW; ++u) {
     if (u >= nvalid) break;
     const int idx = first + u;
     double* dst = partial + ((split * ks + kslice) * g.nst + idx) * 256;
@@ -149,10 +163,21 @@ __global__ void __launch_bounds__(kGrThreads, 1)
     }
   }
   if (do_l1) {
+    if (l1_ph > 1) {  // fixed-order sum of the phases through shared memory
+      __syncthreads();
+      smem[tid] = (l1_r0 < l1_ph) ? l1a[0] : 0.0;
+      __syncthreads();
+      if (tid < g.npad) {
+        double a = 0.0;
+        for (int r = 0; r < l1_ph; ++r) a += smem[r * g.npad + tid];
+        l1part[split * g.npad + tid] = a;
+      }
+    } else {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int col = tid + h * kGrThreads;
-      if (col < g.npad) l1part[split * g.npad + col] = l1a[h];
+      for (int h = 0; h < 2; ++h) {
+        const int col = tid + h * kGrThreads;
+        if (col < g.npad) l1part[split * g.npad + col] = l1a[h];
+      }
     }
   }
 }
@@ -192,9 +217,23 @@ GrGeom gr_geom(int64_t m, int n, int sms) {
   g.lds = smem_stride(g.npad);
   g.ns = g.npad / 16;
   g.nst = g.ns * (g.ns + 1) / 2;
-  g.ks = kGrWarps;  // k-slices: as many as keep every warp busy
-  while (g.ks > 1 && (kGrWarps / g.ks) * kGrSpw < g.nst) g.ks /= 2;
-  g.spc = (kGrWarps / g.ks) * kGrSpw;
+  // Narrow matrices have few super-tiles: pick the per-warp count SPW (a kernel template) and the warps per
+  // k-slice wps (power of two) minimising the DMMA slots issued per k-step, wps * SPW >= nst; the
+  // remaining warps split the rows (ks = 8 / wps k-slices).  Wide ones use SPW = 12, wps = 8 and tile groups.
+  {
+    const int spws[5] = {1, 3, 6, 10, 12};
+    int best_slots = 1 << 30;
+    g.spw = kGrSpwMax;
+    g.ks = 1;
+    for (int wps = 1; wps <= kGrWarps; wps *= 2)
+      for (int i = 0; i < 5; ++i)
+        if (wps * spws[i] >= g.nst && wps * spws[i] < best_slots) {
+          best_slots = wps * spws[i];
+          g.spw = spws[i];
+          g.ks = kGrWarps / wps;
+        }
+  }
+  g.spc = (kGrWarps / g.ks) * g.spw;
   g.groups = (int)ceil_div(g.nst, g.spc);
   g.br = kGrBrMax;
   while (g.br > 8 && 2 * g.br * g.lds * 8 > 227 * 1024) g.br /= 2;
@@ -226,6 +265,19 @@ size_t gram_workspace_bytes(int64_t m, int n) {
   return sizeof(double) * (size_t)(splits * g.ks * g.nst * 256 + splits * g.npad) + 256;
 }
 
+template <int SPW>
+int gram_launch(const double* x, int64_t m, int64_t ldx, const GrGeom& g, double* partial, double* l1part,
+                int64_t splits, size_t smem, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    TSNMF_CUDA_CHECK(cudaFuncSetAttribute(gram_kernel<SPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+    attr = true;
+  }
+  gram_kernel<SPW><<<dim3(g.groups, (unsigned)splits), kGrThreads, smem, st>>>(x, m, ldx, g, partial, l1part);
+  TSNMF_LAUNCH_CHECK();
+  return kOk;
+}
+
 int gram_run(const double* x, int64_t m, int n, int64_t ldx, double* gout, int64_t ldg, double* l1, double* sumsq,
              void* ws, size_t ws_bytes, cudaStream_t st) {
   if (n > gram_max_cols()) return set_error(kUsage, "gram: n = %d exceeds %d", n, gram_max_cols());
@@ -236,15 +288,16 @@ int gram_run(const double* x, int64_t m, int n, int64_t ldx, double* gout, int64
   double* partial = reinterpret_cast<double*>(ws);
   double* l1part = partial + splits * g.ks * g.nst * 256;
   const size_t smem = gr_smem(g);
-  static bool attr = false;
-  if (!attr) {
-    TSNMF_CUDA_CHECK(cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
-    attr = true;
-  }
   prof_mark(kProfGram, true, st);
-  gram_kernel<<<dim3(g.groups, (unsigned)splits), kGrThreads, smem, st>>>(x, m, ldx, g, partial,
-                                                                         l1 ? l1part : nullptr);
-  TSNMF_LAUNCH_CHECK();
+  int rc = kOk;
+  switch (g.spw) {
+    case 1: rc = gram_launch<1>(x, m, ldx, g, partial, l1 ? l1part : nullptr, splits, smem, st); break;
+    case 3: rc = gram_launch<3>(x, m, ldx, g, partial, l1 ? l1part : nullptr, splits, smem, st); break;
+    case 6: rc = gram_launch<6>(x, m, ldx, g, partial, l1 ? l1part : nullptr, splits, smem, st); break;
+    case 10: rc = gram_launch<10>(x, m, ldx, g, partial, l1 ? l1part : nullptr, splits, smem, st); break;
+    default: rc = gram_launch<12>(x, m, ldx, g, partial, l1 ? l1part : nullptr, splits, smem, st); break;
+  }
+  if (rc) return rc;
   prof_mark(kProfGram, false, st);
   gram_reduce_kernel<<<n, 128, 0, st>>>(partial, splits, g, gout, ldg, sumsq);
   TSNMF_LAUNCH_CHECK();
