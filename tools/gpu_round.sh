@@ -14,4 +14,10 @@ python bench.py --rows 4194304 --steps 2 --warmup 1 --no-cpu --no-e2e > gpurun_o
 python tools/run_kernel.py tsqr 2097152 200 1 > gpurun_out/plain.log 2>&1 && \
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:tsqr_leaf -c 1 -o gpurun_out/tsqr_leaf_full \
   python tools/run_kernel.py tsqr 2097152 200 1 > gpurun_out/ncu_full.log 2>&1
+python tools/run_kernel.py gram 4194304 200 1 > gpurun_out/plain_g.log 2>&1 && \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:gram_kernel -c 1 -o gpurun_out/gram_full2 \
+  python tools/run_kernel.py gram 4194304 200 1 > gpurun_out/ncu_full_g.log 2>&1
+python tools/run_kernel.py sketch 1048576 200 1 > gpurun_out/plain_s.log 2>&1 && \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:sketch_gemm -c 1 -o gpurun_out/skgemm_full \
+  python tools/run_kernel.py sketch 1048576 200 1 > gpurun_out/ncu_full_s.log 2>&1
 echo done
