@@ -107,6 +107,10 @@ constexpr bool kLazyPanel = TSNMF_LAZY_PANEL != 0;
 #define TSNMF_HELPER_LOOKAHEAD 1
 #endif
 constexpr bool kHelperLookahead = TSNMF_HELPER_LOOKAHEAD != 0;
+#ifndef TSNMF_PAIR_LOOKAHEAD
+#define TSNMF_PAIR_LOOKAHEAD 1
+#endif
+constexpr bool kPairLookahead = TSNMF_PAIR_LOOKAHEAD != 0;  // panel warp joins the helper's lookahead
 
 // 1/sqrt(a) and 1/a for the Householder scalars: hardware approximation + Newton steps (each doubles the
 // correct bits: ~23 -> ~46 -> full), accurate to ~1 ulp; outside [2^-900, 2^900] (where the .ftz
@@ -550,6 +554,95 @@ __device__ __forceinline__ void lookahead_single(double* __restrict__ Bs, int ld
   }
 }
 
+// Pair lookahead: the panel warp (idle until the next panel's columns are ready) and the helper, both on
+// SMSP 0, apply panel (j0)'s reflector to column block cb together.  Half h takes rows
+// [h*brows/2, (h+1)*brows/2) of GEMM1 (W = R_p + V^T B, 4 accumulator chains; the helper adds the R_p
+// tile), the two partial W tiles meet through shared memory (one 64-thread barrier), both warps form the
+// same W' = T^T W (fixed summation order), the helper writes R_p -= W', and each warp updates its half of
+// the row blocks of B -= V W'.  Two dependency chains interleave on the SMSP's tensor pipe.
+__device__ __forceinline__ void lookahead_pair(double* __restrict__ Bs, int lds, int brows, int j0,
+                                               double* __restrict__ R, int npad, const double* __restrict__ Tm,
+                                               double* __restrict__ Wpart, double* __restrict__ Wsc, int cb, int h,
+                                               int lane) {
+  const int frag_col = (lane >> 2) ^ ((lane & 2) << 1);
+  const int vsw = ((lane >> 2) & 2) << 1;
+  double* rtile = R + (int64_t)(j0 + (lane >> 2)) * npad + 8 * cb + 2 * (lane & 3);
+  double2 rinit = make_double2(0.0, 0.0);
+  if (h == 1) rinit = *reinterpret_cast<const double2*>(rtile);
+  const int nrb = brows / 8;
+  const int rb_mid = nrb / 2;                       // row blocks [0, rb_mid) | [rb_mid, nrb)
+  const int i_beg = h ? 8 * rb_mid : 0, i_end = h ? brows : 8 * rb_mid;
+  double c[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+  const double* slab = Bs + (lane & 3) * lds + frag_col;
+  int i = i_beg;
+#pragma unroll 1
+  for (; i + 16 <= i_end; i += 16) {
+    double a[4], b[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double* r = slab + (i + 4 * u) * lds;
+      a[u] = r[j0];
+      b[u] = r[8 * cb];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) dmma(c[u][0], c[u][1], a[u], b[u]);
+  }
+  for (; i < i_end; i += 4) {
+    const double* r = slab + i * lds;
+    dmma(c[0][0], c[0][1], r[j0], r[8 * cb]);
+  }
+  const int ci = (lane >> 2) * 8 + 2 * (lane & 3);
+  Wpart[h * 64 + ci] = ((c[0][0] + c[1][0]) + (c[2][0] + c[3][0])) + rinit.x;
+  Wpart[h * 64 + ci + 1] = ((c[0][1] + c[1][1]) + (c[2][1] + c[3][1])) + rinit.y;
+  named_sync(kBarPanelPair, 64);
+  Wsc[ci] = Wpart[ci] + Wpart[64 + ci];
+  Wsc[ci + 1] = Wpart[ci + 1] + Wpart[64 + ci + 1];
+  __syncwarp();
+  double w0 = 0.0, w1 = 0.0;
+#pragma unroll
+  for (int k0 = 0; k0 < 8; k0 += 4)
+    dmma(w0, w1, Tm[(k0 + (lane & 3)) * kNB + (lane >> 2)], Wsc[(k0 + (lane & 3)) * 8 + (lane >> 2)]);
+  if (h == 1) {
+    const double2 rv = *reinterpret_cast<const double2*>(rtile);
+    *reinterpret_cast<double2*>(rtile) = make_double2(rv.x - w0, rv.y - w1);
+  }
+  __syncwarp();
+  Wsc[ci] = w0;
+  Wsc[ci + 1] = w1;
+  __syncwarp();
+  const double wb0 = -Wsc[(lane & 3) * 8 + (lane >> 2)];
+  const double wb1 = -Wsc[(4 + (lane & 3)) * 8 + (lane >> 2)];
+  __syncwarp();
+  int rb = h ? rb_mid : 0;
+  const int rb_end = h ? nrb : rb_mid;
+#pragma unroll 1
+  for (; rb + 4 <= rb_end; rb += 4) {
+    double* rows[4];
+    double2 cv[4];
+    double va[4], vb[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      rows[u] = Bs + (8 * (rb + u) + (lane >> 2)) * lds;
+      va[u] = rows[u][j0 + ((lane & 3) ^ vsw)];
+      vb[u] = rows[u][j0 + ((4 + (lane & 3)) ^ vsw)];
+      cv[u] = *reinterpret_cast<const double2*>(rows[u] + 8 * cb + ((2 * (lane & 3)) ^ vsw));
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) dmma(cv[u].x, cv[u].y, va[u], wb0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) dmma(cv[u].x, cv[u].y, vb[u], wb1);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) *reinterpret_cast<double2*>(rows[u] + 8 * cb + ((2 * (lane & 3)) ^ vsw)) = cv[u];
+  }
+  for (; rb < rb_end; ++rb) {
+    double* row = Bs + (8 * rb + (lane >> 2)) * lds;
+    double2 cv = *reinterpret_cast<const double2*>(row + 8 * cb + ((2 * (lane & 3)) ^ vsw));
+    dmma(cv.x, cv.y, row[j0 + ((lane & 3) ^ vsw)], wb0);
+    dmma(cv.x, cv.y, row[j0 + ((4 + (lane & 3)) ^ vsw)], wb1);
+    *reinterpret_cast<double2*>(row + 8 * cb + ((2 * (lane & 3)) ^ vsw)) = cv;
+  }
+}
+
 // Cooperative lookahead: the 6 GEMM warps apply panel (j0)'s reflector to the single column block cb
 // (the next panel's columns).  GEMM1 is split over rows (k-step i/4 = gi mod 6) into 6 partial W tiles
 // summed in fixed order by GEMM warp 0, which also forms W' = T^T W and updates R; then each warp
@@ -685,6 +778,10 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
                                 tq_p);
         TQ_TRACE(2);
         named_arrive(kBarPanelDone, kTqThreads);
+        if (NPW == 1 && kHelperLookahead && kPairLookahead && more) {
+          __syncwarp();  // the warp's own V / T stores are visible to all its lanes
+          lookahead_pair(Bs, lds, brows, j0, R, npad, Tmc, Wpart, Wsc, p + 1, 0, lane);
+        }
       } else if (warp == 4) {
         // NPW == 1: helper on SMSP 0.  While the panel warp waits for ColsReady it is idle, so the helper
         // does the lookahead alone (update of the next panel's column block with panel p) plus the R diag
@@ -696,7 +793,12 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
           TQ_TRACE(3);
           stage_rdiag(Rdg + (buf ^ 1) * kNB * kNB, R, npad, j0 + kNB, lane);
           cp_async_commit();
-          if (kHelperLookahead) lookahead_single(Bs, lds, brows, j0, R, npad, Tmc, Wsc, p + 1, lane);
+          if (kHelperLookahead) {
+            if (kPairLookahead)
+              lookahead_pair(Bs, lds, brows, j0, R, npad, Tmc, Wpart, Wsc, p + 1, 1, lane);
+            else
+              lookahead_single(Bs, lds, brows, j0, R, npad, Tmc, Wsc, p + 1, lane);
+          }
           cp_async_wait<0>();
           __syncwarp();
           TQ_TRACE(4);
