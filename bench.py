@@ -350,6 +350,35 @@ def main():
                           "frac_fp64_gemm_only": sflops / (sk_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
                           "normals_per_s": args.k * (hi - lo) / (sk_ms * 1e-3)}
 
+        # device selection + coefficients (§8f row 1) on this pass's reduced matrix vs the host code
+        if rank == 0:
+            import time as _time
+            from paper_1402_6964_b200 import extremes as _ex, nonneg as _nn
+
+            r_mat, _, _ = dv.tsqr(x)
+            red = tb.rsvd(tb.TriangularFactor(np.triu(r_mat.cpu().numpy())))
+            mat = _ex.as_matrix(red)
+
+            def wall(fn, reps):
+                fn()
+                torch.cuda.synchronize()
+                t0 = _time.perf_counter()
+                for _ in range(reps):
+                    out = fn()
+                torch.cuda.synchronize()
+                return (_time.perf_counter() - t0) * 1e3 / reps, out
+
+            xd_ms, kd = wall(lambda: _ex.xray_order_device(mat, spec.r), 3)
+            hd_ms, hd = wall(lambda: _nn.solve_columns(mat[:, kd], mat, device=True), 3)
+            xh_ms, kh = wall(lambda: _ex.xray_order(mat, spec.r), 1)
+            hh_ms, hh = wall(lambda: _nn.solve_columns(mat[:, kh], mat), 1)
+            line["selection"] = {"workload": f"XRAY r={spec.r} + compute_h on the {n}x{n} reduced matrix of this pass",
+                                 "xray_device_ms": xd_ms, "xray_host_ms": xh_ms,
+                                 "compute_h_device_ms": hd_ms, "compute_h_host_ms": hh_ms,
+                                 "k_identical": list(kd) == list(kh),
+                                 "h_max_abs_diff": float(np.abs(hd - hh).max()) if list(kd) == list(kh) else None,
+                                 "host": "numpy/OpenBLAS Lawson-Hanson (reference algorithm), 1 process"}
+
     # end to end through the public API from pinned host buffers (H2D inside the timed region)
     if not args.no_e2e:
         pool_rows = min(hi - lo, (4 << 30) // (8 * n))

@@ -37,7 +37,8 @@ enum {
   TSNMF_OP_COMBINE = 2, /* m = number of factors, n  */
   TSNMF_OP_GRAM = 3,    /* m rows, n cols            */
   TSNMF_OP_SKETCH = 4,  /* m rows, n cols, k         */
-  TSNMF_OP_STATS = 5    /* m rows, n cols            */
+  TSNMF_OP_STATS = 5,   /* m rows, n cols            */
+  TSNMF_OP_NNLS = 6     /* n = design columns t      */
 };
 
 /* ABI version (bumped on any signature change) and limits. */
@@ -92,6 +93,25 @@ int tsnmf_column_stats(const double* x, int64_t m, int32_t n, int64_t ldx, doubl
 int tsnmf_generate(double* x, int64_t ldx, int64_t row0, int64_t rows, int32_t n, int32_t r,
                    const double* mix, int32_t w_kind, const double* bumps, int64_t m_total, double sigma,
                    uint64_t seed, void* cuda_stream);
+
+/* ---- batched nonnegative least squares: replaces reference pkg/src/tsnmf/nnls.py:47-126 (nnls_solve /
+ *      solve_columns).  For every column j of b (n x ncols, stride ldb): y_j = argmin ||a y - b_j|| with
+ *      y >= 0; a is the n x t design (stride lda, 1 <= t <= tsnmf_nnls_max_cols()), y is t x ncols (stride
+ *      ldy).  Lawson-Hanson with the reference's entering / leaving rules and gradient tolerance `tol`.
+ *      status[j] (device int32 array of ncols): 0 ok, 3 numerical (inner loop failed or singular passive
+ *      set), 5 iteration limit (y_j = last iterate, the reference's NnlsIterationError.best_y). */
+int tsnmf_nnls(const double* a, int64_t n, int32_t t, int64_t lda, const double* b, int64_t ldb, int32_t ncols,
+               double tol, int32_t max_iter, double* y, int64_t ldy, int32_t* status, void* ws, size_t ws_bytes,
+               void* cuda_stream);
+int tsnmf_nnls_max_cols(void);
+
+/* ---- XRAY steps (reference pkg/src/tsnmf/select.py:131-140) on the n x n reduced matrix m (stride ldm):
+ *      scores: score[j] = ||resid^T m(:, j)||_2 / colnorm[j]  (-inf where colnorm[j] <= 0);
+ *      residual: resid = m - a coef, a = m(:, K) (n x t, stride lda), coef t x n (stride ldc). */
+int tsnmf_xray_scores(const double* m, int32_t n, int64_t ldm, const double* resid, int64_t ldr,
+                      const double* colnorm, double* score, void* cuda_stream);
+int tsnmf_xray_residual(const double* m, int32_t n, int64_t ldm, const double* a, int32_t t, int64_t lda,
+                        const double* coef, int64_t ldc, double* resid, int64_t ldr, void* cuda_stream);
 
 /* ---- introspection for benchmarks: chosen TSQR panel width / rows per block / CTAs per SM / leaves */
 int tsnmf_tsqr_plan(int32_t n, int64_t m, int32_t* panel, int32_t* block_rows, int32_t* ctas_per_sm,

@@ -16,7 +16,7 @@ LIB_NAME = "libtsnmf_b200.so"
 LIB_PATH = os.environ.get("TSNMF_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 ABI_VERSION = 1
 
-OP_TSQR, OP_COMBINE, OP_GRAM, OP_SKETCH, OP_STATS = 1, 2, 3, 4, 5
+OP_TSQR, OP_COMBINE, OP_GRAM, OP_SKETCH, OP_STATS, OP_NNLS = 1, 2, 3, 4, 5, 6
 
 _u64, _i64, _i32, _vp, _sz, _dbl = (ctypes.c_uint64, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p,
                                     ctypes.c_size_t, ctypes.c_double)
@@ -37,6 +37,10 @@ SIGNATURES = {
     "tsnmf_sketch": (ctypes.c_int, [_vp, _i64, _i32, _i64, _i64, _u64, _i32, _vp, _i64, _vp, _i64, _vp, _sz, _vp]),
     "tsnmf_column_stats": (ctypes.c_int, [_vp, _i64, _i32, _i64, _vp, _vp, _vp, _sz, _vp]),
     "tsnmf_generate": (ctypes.c_int, [_vp, _i64, _i64, _i64, _i32, _i32, _vp, _i32, _vp, _i64, _dbl, _u64, _vp]),
+    "tsnmf_nnls": (ctypes.c_int, [_vp, _i64, _i32, _i64, _vp, _i64, _i32, _dbl, _i32, _vp, _i64, _vp, _vp, _sz, _vp]),
+    "tsnmf_nnls_max_cols": (ctypes.c_int, []),
+    "tsnmf_xray_scores": (ctypes.c_int, [_vp, _i32, _i64, _vp, _i64, _vp, _vp, _vp]),
+    "tsnmf_xray_residual": (ctypes.c_int, [_vp, _i32, _i64, _vp, _i32, _i64, _vp, _i64, _vp, _i64, _vp]),
     "tsnmf_launch_count": (ctypes.c_longlong, []),
     "tsnmf_profile_enable": (ctypes.c_int, [ctypes.c_int]),
     "tsnmf_profile_read": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double),

@@ -85,6 +85,7 @@ size_t tsnmf_workspace_bytes(int op, int64_t m, int32_t n, int32_t k) {
     case TSNMF_OP_GRAM: return gram_workspace_bytes(m, n);
     case TSNMF_OP_SKETCH: return sketch_workspace_bytes(m, n, k);
     case TSNMF_OP_STATS: return stats_workspace_bytes(m, n);
+    case TSNMF_OP_NNLS: return nnls_workspace_bytes(n);
     default: return 0;
   }
 }
@@ -162,6 +163,34 @@ int tsnmf_generate(double* x, int64_t ldx, int64_t row0, int64_t rows, int32_t n
   if (!x || !mix || ldx < n) return set_error(kUsage, "generate: bad pointers or stride");
   if (sigma < 0) return set_error(kUsage, "generate: negative noise level");
   return generate_run(x, ldx, row0, rows, n, r, mix, w_kind, bumps, m_total, sigma, seed, as_stream(s));
+}
+
+int tsnmf_nnls(const double* a, int64_t n, int32_t t, int64_t lda, const double* b, int64_t ldb, int32_t ncols,
+               double tol, int32_t max_iter, double* y, int64_t ldy, int32_t* status, void* ws, size_t ws_bytes,
+               void* s) {
+  if (int rc = check_matrix("nnls", a, n, t, lda)) return rc;
+  if (ncols < 1) return set_error(kUsage, "nnls: need at least one target column");
+  if (!b || ldb < ncols) return set_error(kUsage, "nnls: bad targets pointer / stride");
+  if (!y || ldy < ncols || !status) return set_error(kUsage, "nnls: bad output pointers / stride");
+  if (!(tol >= 0.0) || max_iter < 1) return set_error(kUsage, "nnls: need tol >= 0 and max_iter >= 1");
+  return nnls_run(a, n, t, lda, b, ldb, ncols, tol, max_iter, y, ldy, status, ws, ws_bytes, as_stream(s));
+}
+
+int tsnmf_nnls_max_cols(void) { return nnls_max_design_cols(); }
+
+int tsnmf_xray_scores(const double* m, int32_t n, int64_t ldm, const double* resid, int64_t ldr,
+                      const double* colnorm, double* score, void* s) {
+  if (int rc = check_matrix("xray_scores", m, n, n, ldm)) return rc;
+  if (!resid || ldr < n || !colnorm || !score) return set_error(kUsage, "xray_scores: bad pointers / stride");
+  return xray_scores_run(m, n, ldm, resid, ldr, colnorm, score, as_stream(s));
+}
+
+int tsnmf_xray_residual(const double* m, int32_t n, int64_t ldm, const double* a, int32_t t, int64_t lda,
+                        const double* coef, int64_t ldc, double* resid, int64_t ldr, void* s) {
+  if (int rc = check_matrix("xray_residual", m, n, n, ldm)) return rc;
+  if (t < 1 || !a || lda < t || !coef || ldc < n || !resid || ldr < n)
+    return set_error(kUsage, "xray_residual: bad design / coefficient / output arguments");
+  return xray_residual_run(m, n, ldm, a, t, lda, coef, ldc, resid, ldr, as_stream(s));
 }
 
 long long tsnmf_launch_count(void) { return g_launches.load(); }

@@ -20,6 +20,15 @@ int r_combine_run(const double* rs, int count, int n, double* r, int64_t ldr, vo
                   cudaStream_t st);
 int tsqr_describe(int n, int64_t m, int* nb, int* brows, int* ctas_per_sm, int* nleaves);
 
+size_t nnls_workspace_bytes(int t);
+int nnls_max_design_cols();
+int nnls_run(const double* a, int64_t n, int t, int64_t lda, const double* b, int64_t ldb, int ncols, double tol,
+             int max_iter, double* y, int64_t ldy, int* status, void* ws, size_t ws_bytes, cudaStream_t st);
+int xray_scores_run(const double* m, int n, int64_t ldm, const double* resid, int64_t ldr, const double* colnorm,
+                    double* score, cudaStream_t st);
+int xray_residual_run(const double* m, int n, int64_t ldm, const double* a, int t, int64_t lda, const double* coef,
+                      int64_t ldc, double* resid, int64_t ldr, cudaStream_t st);
+
 int gram_max_cols();
 size_t gram_workspace_bytes(int64_t m, int n);
 int gram_run(const double* x, int64_t m, int n, int64_t ldx, double* g, int64_t ldg, double* l1, double* sumsq,

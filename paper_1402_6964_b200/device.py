@@ -197,6 +197,52 @@ def column_stats(x):
 
 
 # ---------------------------------------------------------------------------
+# selection / coefficients
+
+
+def nnls(a, b, *, tol: float = 1e-8, max_iter: int = 10_000):
+    """Batched NNLS on the device: Y[:, j] = argmin ||a y - b[:, j]||, y >= 0 (reference nnls.py:47-126).
+    a: n x t design, b: n x ncols targets (host or device).  Returns (Y t x ncols, status ncols) device
+    tensors; status 0 ok, 3 numerical, 5 iteration limit."""
+    t = torch()
+    a = as_device_matrix(a)
+    dev = a.device
+    b = as_device_matrix(b, dev)
+    n, q = int(a.shape[0]), int(a.shape[1])
+    if int(b.shape[0]) != n:
+        raise UsageError(f"incompatible shapes {tuple(a.shape)} and {tuple(b.shape)}", stage="nnls")
+    ncols = int(b.shape[1])
+    y = t.empty((q, ncols), dtype=t.float64, device=dev)
+    status = t.empty(ncols, dtype=t.int32, device=dev)
+    ws, wsb = _workspace(_native.OP_NNLS, 1, q, 0, dev)
+    _native.call("tsnmf_nnls", a.data_ptr(), n, q, _ld(a), b.data_ptr(), _ld(b), ncols, float(tol), int(max_iter),
+                 y.data_ptr(), ncols, status.data_ptr(), ws, wsb, stream_ptr(dev), stage="nnls")
+    return y, status
+
+
+def nnls_max_cols() -> int:
+    return int(_native.load().tsnmf_nnls_max_cols())
+
+
+def xray_scores(m, resid, colnorm):
+    """score[j] = ||resid^T m[:, j]|| / colnorm[j] (-inf where colnorm <= 0) (reference select.py:131-135)."""
+    t = torch()
+    n = int(m.shape[0])
+    score = t.empty(n, dtype=t.float64, device=m.device)
+    _native.call("tsnmf_xray_scores", m.data_ptr(), n, _ld(m), resid.data_ptr(), _ld(resid), colnorm.data_ptr(),
+                 score.data_ptr(), stream_ptr(m.device), stage="xray")
+    return score
+
+
+def xray_residual(m, a, coef, out):
+    """out = m - a @ coef (reference select.py:138-140)."""
+    n, q = int(m.shape[0]), int(a.shape[1])
+    _native.call("tsnmf_xray_residual", m.data_ptr(), n, _ld(m), a.data_ptr(), q, _ld(a), coef.data_ptr(),
+                 _ld(coef), out.data_ptr(), _ld(out), stream_ptr(m.device), stage="xray")
+    return out
+
+
+# ---------------------------------------------------------------------------
 # counter RNG blocks
 
 
