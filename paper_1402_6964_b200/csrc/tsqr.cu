@@ -889,6 +889,128 @@ __global__ void __launch_bounds__(kTqThreads, MINB)
   tsqr_fold<RQ, NPW>(slots + dst * ss, slots + srcs * ss, g.npad, g.npad, g.npad, g, true, false, nullptr, smem);
 }
 
+// ---------------------------------------------------------------------------
+// Narrow leaf (n <= 32, e.g. config C4 n = 25): one WARP per chain.  Each warp owns a contiguous row range
+// and its own R (lane c holds column c of R in registers), stages 32-row blocks in shared memory
+// (cp.async), takes row l of the block into lane l's registers and folds it into R with Householder
+// reflectors [e_j; v] one column at a time:
+//   norm: warp butterfly;  scalars (dlarfg conventions, as the panel);  v_l = x_l[j] * scale;
+//   w_c = R(j, c) + sum_l v_l x_l[c]  (lane c sums the column of products through shared memory);
+//   R(j, c) -= tau w_c (lane c);  x_l[c] -= tau w_c v_l (every lane, row l).
+// No CTA barriers, no panel/GEMM split: the shared-panel design's throughput is bounded by one panel
+// chain per SM (rows in flight / (n x column latency)); here 12 independent chains per SM run in parallel
+// (3 CTAs x 4 warps) and the kernel is issue-bound instead.  Leaves = warps, combined by the same tree.
+constexpr int kSmWarps = 4;
+
+template <int NC>
+struct SmallLayout {
+  static constexpr int ld = NC + 1;                 // odd stride: column reads by lane c are conflict-free
+  static constexpr int per_warp = 32 * ld;          // staged block / products (doubles)
+  static constexpr size_t bytes = sizeof(double) * (size_t)per_warp * kSmWarps;
+};
+
+template <int NC>
+__global__ void __launch_bounds__(32 * kSmWarps, 3)
+    tsqr_small_leaf_kernel(const double* __restrict__ x, int64_t m, int n, int64_t ldx, int64_t rows_per_warp,
+                           int npad, double* __restrict__ slots, double* __restrict__ stats) {
+  extern __shared__ __align__(16) double smem[];
+  using Ly = SmallLayout<NC>;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t leaf = (int64_t)blockIdx.x * kSmWarps + wib;
+  double* buf = smem + wib * Ly::per_warp;
+  const int64_t rbeg = leaf * rows_per_warp;
+  const int64_t rend = min64(m, rbeg + rows_per_warp);
+  double rcol[NC];  // lane c: column c of R (rows 0..NC)
+#pragma unroll
+  for (int i = 0; i < NC; ++i) rcol[i] = 0.0;
+  double l1 = 0.0, sq = 0.0;  // lane c: column c
+  for (int64_t r0 = rbeg; r0 < rend; r0 += 32) {
+    const int cnt = (int)min64(32, rend - r0);
+    // stage rows [r0, r0 + cnt) (zero-padded to 32 x NC); element (row, c) at buf[row * ld + c]
+    __syncwarp();
+    for (int idx = lane; idx < 32 * NC; idx += 32) {
+      const int row = idx / NC, c = idx - row * NC;
+      if (row < cnt && c < n)
+        cp_async8(buf + row * Ly::ld + c, x + (r0 + row) * ldx + c);
+      else
+        buf[row * Ly::ld + c] = 0.0;
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncwarp();
+    if (lane < NC) {
+      double a = 0.0, q = 0.0;
+#pragma unroll 8
+      for (int row = 0; row < 32; ++row) {
+        const double v = buf[row * Ly::ld + lane];
+        a += fabs(v);
+        q = fma(v, v, q);
+      }
+      l1 += a;
+      sq += q;
+    }
+    double xr[NC];  // lane l: row l of the block
+#pragma unroll
+    for (int c = 0; c < NC; ++c) xr[c] = buf[lane * Ly::ld + c];
+    __syncwarp();  // buf is reused for the products below
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      if (j >= n) break;
+      // sub-column norm^2 and alpha = R(j, j) (lane j)
+      double d = xr[j] * xr[j];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+      const double alpha = __shfl_sync(0xffffffffu, rcol[j], j);
+      double tau = 0.0, scale = 0.0, beta = alpha;
+      if (d > 0.0) {
+        const double ss = fma(alpha, alpha, d);
+        const double inv = fast_rsqrt(ss);
+        const double nrm = ss * inv;
+        beta = -copysign(nrm, alpha);
+        tau = fma(fabs(alpha), inv, 1.0);
+        scale = copysign(fast_rcp(fabs(alpha) + nrm), alpha);
+      }
+      const double v = xr[j] * scale;
+      __syncwarp();  // every lane has read the previous column's tw values from buf
+      // products P[l][c] = v_l x_l[c] for c > j; lane c sums its column
+#pragma unroll
+      for (int c = j + 1; c < NC; ++c) buf[lane * Ly::ld + c] = v * xr[c];
+      __syncwarp();
+      double tw = 0.0;
+      if (lane > j && lane < NC) {
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+        for (int row = 0; row < 32; row += 4) {
+          s0 += buf[(row + 0) * Ly::ld + lane];
+          s1 += buf[(row + 1) * Ly::ld + lane];
+          s2 += buf[(row + 2) * Ly::ld + lane];
+          s3 += buf[(row + 3) * Ly::ld + lane];
+        }
+        const double w = rcol[j] + ((s0 + s1) + (s2 + s3));
+        tw = tau * w;
+        rcol[j] -= tw;
+      }
+      if (lane == j) rcol[j] = beta;
+      __syncwarp();  // products consumed
+      if (lane > j && lane < NC) buf[lane] = tw;  // row 0 of the product tile is free now
+      __syncwarp();
+#pragma unroll
+      for (int c = j + 1; c < NC; ++c) xr[c] = fma(-buf[c], v, xr[c]);  // broadcast reads
+    }
+  }
+  double* R = slots + leaf * npad * npad;
+  if (lane < npad) {
+#pragma unroll
+    for (int i = 0; i < NC; ++i)
+      if (i < npad) R[(int64_t)i * npad + lane] = (i <= lane && lane < n) ? rcol[i] : 0.0;
+    for (int i = NC; i < npad; ++i) R[(int64_t)i * npad + lane] = 0.0;
+    if (stats) {
+      stats[leaf * 2 * npad + lane] = lane < n ? l1 : 0.0;
+      stats[leaf * 2 * npad + npad + lane] = lane < n ? sq : 0.0;
+    }
+  }
+}
+
 // R_out (n x n, row-major, stride ldr) = sign-fixed upper triangle of slot 0 (tsqr.py:113-118).
 __global__ void tsqr_finalize_kernel(const double* __restrict__ slot, int npad, int n, double* __restrict__ r,
                                      int64_t ldr) {
@@ -1051,6 +1173,47 @@ void tq_plan(const TqChoice& ch, int64_t m, int* nleaves, int64_t* rows_per_cta)
   *rows_per_cta = rpc;
 }
 
+// Narrow leaf plan (n <= 32): one chain per warp, 3 CTAs x 4 warps per SM, 32-row blocks.
+bool small_path(int n) {
+  if (n > 32) return false;
+  if (const char* e = getenv("TSNMF_TSQR_SMALL")) return atoi(e) != 0;
+  return true;
+}
+
+void small_plan(int64_t m, int* nleaves, int64_t* rows_per_warp) {
+  const int64_t max_leaves = (int64_t)device_sms() * 3 * kSmWarps;
+  int64_t leaves = max64(1, min64(max_leaves, ceil_div(m, 32)));
+  const int64_t rpw = round_up(ceil_div(m, leaves), 32);
+  leaves = round_up(ceil_div(m, rpw), kSmWarps);  // whole CTAs; surplus warps contribute zero factors
+  *nleaves = (int)leaves;
+  *rows_per_warp = rpw;
+}
+
+template <int NC>
+int small_launch(const double* x, int64_t m, int n, int64_t ldx, int64_t rpw, int nleaves, int npad, double* slots,
+                 double* stats, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    TSNMF_CUDA_CHECK(cudaFuncSetAttribute(tsqr_small_leaf_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)SmallLayout<NC>::bytes));
+    attr = true;
+  }
+  tsqr_small_leaf_kernel<NC><<<nleaves / kSmWarps, 32 * kSmWarps, SmallLayout<NC>::bytes, st>>>(
+      x, m, n, ldx, rpw, npad, slots, stats);
+  TSNMF_LAUNCH_CHECK();
+  return kOk;
+}
+
+int small_leaf(const double* x, int64_t m, int n, int64_t ldx, int64_t rpw, int nleaves, int npad, double* slots,
+               double* stats, cudaStream_t st) {
+  switch (npad) {
+    case 8: return small_launch<8>(x, m, n, ldx, rpw, nleaves, npad, slots, stats, st);
+    case 16: return small_launch<16>(x, m, n, ldx, rpw, nleaves, npad, slots, stats, st);
+    case 24: return small_launch<24>(x, m, n, ldx, rpw, nleaves, npad, slots, stats, st);
+    default: return small_launch<32>(x, m, n, ldx, rpw, nleaves, npad, slots, stats, st);
+  }
+}
+
 }  // namespace
 
 int tsqr_max_cols() { return 512; }
@@ -1071,7 +1234,10 @@ size_t tsqr_workspace_bytes(int64_t m, int n) {
   if (n < 1 || !tq_config(n, &ch)) return 0;
   int nleaves;
   int64_t rpc;
-  tq_plan(ch, max64(m, 1), &nleaves, &rpc);
+  if (small_path(n))
+    small_plan(max64(m, 1), &nleaves, &rpc);
+  else
+    tq_plan(ch, max64(m, 1), &nleaves, &rpc);
   const int64_t npad = ch.g.npad;
   return sizeof(double) * (size_t)(nleaves * npad * npad + nleaves * 2 * npad) + 256;
 }
@@ -1089,14 +1255,26 @@ int tsqr_run(const double* x, int64_t m, int n, int64_t ldx, double* r, int64_t 
   if (!tq_config(n, &ch)) return set_error(kUsage, "tsqr: n = %d columns does not fit the on-chip block", n);
   int nleaves;
   int64_t rpc;
-  tq_plan(ch, m, &nleaves, &rpc);
+  const bool narrow = small_path(n);
+  if (narrow)
+    small_plan(m, &nleaves, &rpc);
+  else
+    tq_plan(ch, m, &nleaves, &rpc);
   const int64_t npad = ch.g.npad;
   const size_t need = sizeof(double) * (size_t)(nleaves * npad * npad + nleaves * 2 * npad);
   if (ws_bytes < need) return set_error(kUsage, "tsqr: workspace too small (%zu < %zu bytes)", ws_bytes, need);
   double* slots = reinterpret_cast<double*>(ws);
   double* stats = slots + (int64_t)nleaves * npad * npad;
   const bool want_stats = (l1 != nullptr) || (sumsq != nullptr);
-  int rc = tq_dispatch(ch, x, m, ldx, slots, want_stats ? stats : nullptr, nleaves, rpc, st);
+  int rc;
+  if (narrow) {
+    prof_mark(kProfTsqrLeaf, true, st);
+    rc = small_leaf(x, m, n, ldx, rpc, nleaves, (int)npad, slots, want_stats ? stats : nullptr, st);
+    prof_mark(kProfTsqrLeaf, false, st);
+    if (!rc) rc = tq_dispatch(ch, nullptr, 0, 0, slots, nullptr, nleaves, 0, st);  // combine tree only
+  } else {
+    rc = tq_dispatch(ch, x, m, ldx, slots, want_stats ? stats : nullptr, nleaves, rpc, st);
+  }
   if (rc) return rc;
   tsqr_finalize_kernel<<<n, 128, 0, st>>>(slots, (int)npad, n, r, ldr);
   TSNMF_LAUNCH_CHECK();
@@ -1128,6 +1306,13 @@ int tsqr_describe(int n, int64_t m, int* nb, int* brows, int* ctas_per_sm, int* 
   TqChoice ch;
   if (!tq_config(n, &ch)) return set_error(kUsage, "tsqr: n = %d too large", n);
   int64_t rpc;
+  if (small_path(n)) {  // warp-per-chain leaf: "panel" 1 column, 32-row blocks, 3 CTAs (12 chains) per SM
+    small_plan(max64(m, 1), nleaves, &rpc);
+    *nb = 1;
+    *brows = 32;
+    *ctas_per_sm = 3;
+    return kOk;
+  }
   tq_plan(ch, max64(m, 1), nleaves, &rpc);
   *nb = kNB;
   *brows = ch.g.brows;
