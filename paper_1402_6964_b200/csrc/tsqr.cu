@@ -909,6 +909,96 @@ struct SmallLayout {
   static constexpr size_t bytes = sizeof(double) * (size_t)per_warp * kSmWarps;
 };
 
+// Fold rows [0, cnt) (cnt <= 32) of a row-major matrix (stride ld, n real columns) into the warp's R
+// (lane c holds column c).  buf: the warp's 32 x (NC+1) shared tile.  With `l1`/`sq` set, lane c also
+// accumulates the column's sum of |x| and x^2.
+template <int NC>
+__device__ __forceinline__ void small_fold_block(const double* __restrict__ src, int64_t ld, int cnt, int n,
+                                                 double* __restrict__ buf, double (&rcol)[NC], int lane,
+                                                 double* l1, double* sq) {
+  using Ly = SmallLayout<NC>;
+  // stage (zero-padded to 32 x NC); element (row, c) at buf[row * ld + c]
+  __syncwarp();
+  for (int idx = lane; idx < 32 * NC; idx += 32) {
+    const int row = idx / NC, c = idx - row * NC;
+    if (row < cnt && c < n)
+      cp_async8(buf + row * Ly::ld + c, src + row * ld + c);
+    else
+      buf[row * Ly::ld + c] = 0.0;
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncwarp();
+  if (l1 && lane < NC) {
+    double a = 0.0, q = 0.0;
+#pragma unroll 8
+    for (int row = 0; row < 32; ++row) {
+      const double v = buf[row * Ly::ld + lane];
+      a += fabs(v);
+      q = fma(v, v, q);
+    }
+    *l1 += a;
+    *sq += q;
+  }
+  double xr[NC];  // lane l: row l of the block
+#pragma unroll
+  for (int c = 0; c < NC; ++c) xr[c] = buf[lane * Ly::ld + c];
+#pragma unroll
+  for (int j = 0; j < NC; ++j) {
+    if (j >= n) break;
+    // sub-column norm^2 and alpha = R(j, j) (lane j)
+    double d = xr[j] * xr[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+    const double alpha = __shfl_sync(0xffffffffu, rcol[j], j);
+    double tau = 0.0, scale = 0.0, beta = alpha;
+    if (d > 0.0) {
+      const double ss = fma(alpha, alpha, d);
+      const double inv = fast_rsqrt(ss);
+      const double nrm = ss * inv;
+      beta = -copysign(nrm, alpha);
+      tau = fma(fabs(alpha), inv, 1.0);
+      scale = copysign(fast_rcp(fabs(alpha) + nrm), alpha);
+    }
+    const double v = xr[j] * scale;
+    __syncwarp();  // every lane has read the previous column's tw values from buf
+    // products P[l][c] = v_l x_l[c] for c > j; lane c sums its column
+#pragma unroll
+    for (int c = j + 1; c < NC; ++c) buf[lane * Ly::ld + c] = v * xr[c];
+    __syncwarp();
+    double tw = 0.0;
+    if (lane > j && lane < NC) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+      for (int row = 0; row < 32; row += 4) {
+        s0 += buf[(row + 0) * Ly::ld + lane];
+        s1 += buf[(row + 1) * Ly::ld + lane];
+        s2 += buf[(row + 2) * Ly::ld + lane];
+        s3 += buf[(row + 3) * Ly::ld + lane];
+      }
+      const double w = rcol[j] + ((s0 + s1) + (s2 + s3));
+      tw = tau * w;
+      rcol[j] -= tw;
+    }
+    if (lane == j) rcol[j] = beta;
+    __syncwarp();  // products consumed
+    if (lane > j && lane < NC) buf[lane] = tw;  // row 0 of the product tile is free now
+    __syncwarp();
+#pragma unroll
+    for (int c = j + 1; c < NC; ++c) xr[c] = fma(-buf[c], v, xr[c]);  // broadcast reads
+  }
+}
+
+template <int NC>
+__device__ __forceinline__ void small_store_r(double* __restrict__ R, int npad, int n, const double (&rcol)[NC],
+                                              int lane) {
+  if (lane < npad) {
+#pragma unroll
+    for (int i = 0; i < NC; ++i)
+      if (i < npad) R[(int64_t)i * npad + lane] = (i <= lane && lane < n) ? rcol[i] : 0.0;
+  }
+}
+
 template <int NC>
 __global__ void __launch_bounds__(32 * kSmWarps, 3)
     tsqr_small_leaf_kernel(const double* __restrict__ x, int64_t m, int n, int64_t ldx, int64_t rows_per_warp,
@@ -924,91 +1014,36 @@ __global__ void __launch_bounds__(32 * kSmWarps, 3)
 #pragma unroll
   for (int i = 0; i < NC; ++i) rcol[i] = 0.0;
   double l1 = 0.0, sq = 0.0;  // lane c: column c
-  for (int64_t r0 = rbeg; r0 < rend; r0 += 32) {
-    const int cnt = (int)min64(32, rend - r0);
-    // stage rows [r0, r0 + cnt) (zero-padded to 32 x NC); element (row, c) at buf[row * ld + c]
-    __syncwarp();
-    for (int idx = lane; idx < 32 * NC; idx += 32) {
-      const int row = idx / NC, c = idx - row * NC;
-      if (row < cnt && c < n)
-        cp_async8(buf + row * Ly::ld + c, x + (r0 + row) * ldx + c);
-      else
-        buf[row * Ly::ld + c] = 0.0;
-    }
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncwarp();
-    if (lane < NC) {
-      double a = 0.0, q = 0.0;
-#pragma unroll 8
-      for (int row = 0; row < 32; ++row) {
-        const double v = buf[row * Ly::ld + lane];
-        a += fabs(v);
-        q = fma(v, v, q);
-      }
-      l1 += a;
-      sq += q;
-    }
-    double xr[NC];  // lane l: row l of the block
-#pragma unroll
-    for (int c = 0; c < NC; ++c) xr[c] = buf[lane * Ly::ld + c];
-    __syncwarp();  // buf is reused for the products below
-#pragma unroll
-    for (int j = 0; j < NC; ++j) {
-      if (j >= n) break;
-      // sub-column norm^2 and alpha = R(j, j) (lane j)
-      double d = xr[j] * xr[j];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-      const double alpha = __shfl_sync(0xffffffffu, rcol[j], j);
-      double tau = 0.0, scale = 0.0, beta = alpha;
-      if (d > 0.0) {
-        const double ss = fma(alpha, alpha, d);
-        const double inv = fast_rsqrt(ss);
-        const double nrm = ss * inv;
-        beta = -copysign(nrm, alpha);
-        tau = fma(fabs(alpha), inv, 1.0);
-        scale = copysign(fast_rcp(fabs(alpha) + nrm), alpha);
-      }
-      const double v = xr[j] * scale;
-      __syncwarp();  // every lane has read the previous column's tw values from buf
-      // products P[l][c] = v_l x_l[c] for c > j; lane c sums its column
-#pragma unroll
-      for (int c = j + 1; c < NC; ++c) buf[lane * Ly::ld + c] = v * xr[c];
-      __syncwarp();
-      double tw = 0.0;
-      if (lane > j && lane < NC) {
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-        for (int row = 0; row < 32; row += 4) {
-          s0 += buf[(row + 0) * Ly::ld + lane];
-          s1 += buf[(row + 1) * Ly::ld + lane];
-          s2 += buf[(row + 2) * Ly::ld + lane];
-          s3 += buf[(row + 3) * Ly::ld + lane];
-        }
-        const double w = rcol[j] + ((s0 + s1) + (s2 + s3));
-        tw = tau * w;
-        rcol[j] -= tw;
-      }
-      if (lane == j) rcol[j] = beta;
-      __syncwarp();  // products consumed
-      if (lane > j && lane < NC) buf[lane] = tw;  // row 0 of the product tile is free now
-      __syncwarp();
-#pragma unroll
-      for (int c = j + 1; c < NC; ++c) xr[c] = fma(-buf[c], v, xr[c]);  // broadcast reads
-    }
+  for (int64_t r0 = rbeg; r0 < rend; r0 += 32)
+    small_fold_block<NC>(x + r0 * ldx, ldx, (int)min64(32, rend - r0), n, buf, rcol, lane, stats ? &l1 : nullptr,
+                         &sq);
+  small_store_r<NC>(slots + leaf * npad * npad, npad, n, rcol, lane);
+  if (stats && lane < npad) {
+    stats[leaf * 2 * npad + lane] = lane < n ? l1 : 0.0;
+    stats[leaf * 2 * npad + npad + lane] = lane < n ? sq : 0.0;
   }
-  double* R = slots + leaf * npad * npad;
-  if (lane < npad) {
+}
+
+// One level of the binary-counter tree for the narrow path, one warp per pair:
+// slot[q span] = qr([slot[q span]; slot[q span + half]]), or (span == 0) slot[dst] = qr([slot[dst]; slot[src]]).
+template <int NC>
+__global__ void __launch_bounds__(32 * kSmWarps)
+    tsqr_small_combine_kernel(double* __restrict__ slots, int npad, int n, int64_t span, int64_t half, int64_t npairs,
+                              int64_t fold_dst, int64_t fold_src) {
+  extern __shared__ __align__(16) double smem[];
+  using Ly = SmallLayout<NC>;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t q = (int64_t)blockIdx.x * kSmWarps + wib;
+  if (span > 0 && q >= npairs) return;  // whole idle warps only (no CTA barrier in this kernel)
+  const int64_t dst = span > 0 ? q * span : fold_dst;
+  const int64_t src = span > 0 ? dst + half : fold_src;
+  const int64_t ss = (int64_t)npad * npad;
+  double* R = slots + dst * ss;
+  double rcol[NC];
 #pragma unroll
-    for (int i = 0; i < NC; ++i)
-      if (i < npad) R[(int64_t)i * npad + lane] = (i <= lane && lane < n) ? rcol[i] : 0.0;
-    for (int i = NC; i < npad; ++i) R[(int64_t)i * npad + lane] = 0.0;
-    if (stats) {
-      stats[leaf * 2 * npad + lane] = lane < n ? l1 : 0.0;
-      stats[leaf * 2 * npad + npad + lane] = lane < n ? sq : 0.0;
-    }
-  }
+  for (int i = 0; i < NC; ++i) rcol[i] = (i < npad && lane < npad) ? R[(int64_t)i * npad + lane] : 0.0;
+  small_fold_block<NC>(slots + src * ss, npad, npad, n, smem + wib * Ly::per_warp, rcol, lane, nullptr, nullptr);
+  small_store_r<NC>(R, npad, n, rcol, lane);
 }
 
 // R_out (n x n, row-major, stride ldr) = sign-fixed upper triangle of slot 0 (tsqr.py:113-118).
@@ -1198,9 +1233,32 @@ int small_launch(const double* x, int64_t m, int n, int64_t ldx, int64_t rpw, in
                                           (int)SmallLayout<NC>::bytes));
     attr = true;
   }
+  prof_mark(kProfTsqrLeaf, true, st);
   tsqr_small_leaf_kernel<NC><<<nleaves / kSmWarps, 32 * kSmWarps, SmallLayout<NC>::bytes, st>>>(
       x, m, n, ldx, rpw, npad, slots, stats);
   TSNMF_LAUNCH_CHECK();
+  prof_mark(kProfTsqrLeaf, false, st);
+  // binary-counter tree (tsqr.py:213-230): perfect levels, then fold leftover subtrees low -> high
+  prof_mark(kProfTsqrTree, true, st);
+  for (int64_t span = 2; span <= nleaves; span *= 2) {
+    const int64_t pairs = nleaves / span;
+    tsqr_small_combine_kernel<NC><<<(unsigned)ceil_div(pairs, kSmWarps), 32 * kSmWarps, SmallLayout<NC>::bytes, st>>>(
+        slots, npad, n, span, span / 2, pairs, 0, 0);
+    TSNMF_LAUNCH_CHECK();
+  }
+  int64_t offs[64];
+  int nsub = 0;
+  int64_t o = 0;
+  for (int b = 62; b >= 0; --b)
+    if ((int64_t)nleaves & (1LL << b)) {
+      offs[nsub++] = o;
+      o += (1LL << b);
+    }
+  for (int t = nsub - 2; t >= 0; --t) {
+    tsqr_small_combine_kernel<NC><<<1, 32, SmallLayout<NC>::bytes, st>>>(slots, npad, n, 0, 0, 0, offs[t], offs[t + 1]);
+    TSNMF_LAUNCH_CHECK();
+  }
+  prof_mark(kProfTsqrTree, false, st);
   return kOk;
 }
 
@@ -1268,10 +1326,7 @@ int tsqr_run(const double* x, int64_t m, int n, int64_t ldx, double* r, int64_t 
   const bool want_stats = (l1 != nullptr) || (sumsq != nullptr);
   int rc;
   if (narrow) {
-    prof_mark(kProfTsqrLeaf, true, st);
     rc = small_leaf(x, m, n, ldx, rpc, nleaves, (int)npad, slots, want_stats ? stats : nullptr, st);
-    prof_mark(kProfTsqrLeaf, false, st);
-    if (!rc) rc = tq_dispatch(ch, nullptr, 0, 0, slots, nullptr, nleaves, 0, st);  // combine tree only
   } else {
     rc = tq_dispatch(ch, x, m, ldx, slots, want_stats ? stats : nullptr, nleaves, rpc, st);
   }
