@@ -20,6 +20,10 @@
 
 namespace tsnmf {
 
+#ifndef TSNMF_HELPER_LOOKAHEAD
+#define TSNMF_HELPER_LOOKAHEAD 1
+#endif
+
 constexpr int kTqThreads = 256;
 constexpr int kTqWarps = kTqThreads / 32;
 constexpr int kNB = 8;       // panel width (reflectors per compact-WY block)
@@ -30,17 +34,21 @@ struct TqGeom {
   int npad;   // padded columns (multiple of 8); R slots are npad x npad
   int lds;    // shared-memory row stride of the block (% 16 == 8)
   int brows;  // rows per block (multiple of 8, <= 64 * kMaxRq)
+  int npw;    // panel warps (1: lean layout — one reduction scratch, pair-lookahead partials only)
 };
 
 struct TqLayout {
   // offsets in doubles from the dynamic smem base
   __host__ __device__ static int rd(const TqGeom& g) { return g.brows * g.lds; }            // 2 x 8x8 R diag blocks
   __host__ __device__ static int tm(const TqGeom& g) { return rd(g) + 2 * kNB * kNB; }      // 2 x 8x8 T
-  __host__ __device__ static int red(const TqGeom& g) { return tm(g) + 2 * kNB * kNB; }    // 2 x 32 x 9 partials
-  __host__ __device__ static int xch(const TqGeom& g) { return red(g) + 2 * 32 * 9; }       // 2 x 16 exchange
+  __host__ __device__ static int red(const TqGeom& g) { return tm(g) + 2 * kNB * kNB; }    // npw x 32 x 9 partials
+  __host__ __device__ static int xch(const TqGeom& g) { return red(g) + g.npw * 32 * 9; }  // 2 x 16 exchange
   __host__ __device__ static int wsc(const TqGeom& g) { return xch(g) + 32; }                // per-warp 8x8 scratch
-  __host__ __device__ static int wpart(const TqGeom& g) { return wsc(g) + kTqWarps * kNB * 8; }  // 6 partial W + W'
-  __host__ __device__ static int total(const TqGeom& g) { return wpart(g) + 7 * 64; }
+  __host__ __device__ static int wpart(const TqGeom& g) { return wsc(g) + kTqWarps * kNB * 8; }  // partial W tiles
+  // 6 partial W + W' for the cooperative lookahead (NPW == 2), 2 for the pair lookahead (NPW == 1)
+  __host__ __device__ static int total(const TqGeom& g) {
+    return wpart(g) + ((g.npw == 2 || TSNMF_HELPER_LOOKAHEAD == 0) ? 7 : 2) * 64;
+  }
   static size_t bytes(const TqGeom& g) { return sizeof(double) * (size_t)total(g); }
 };
 
@@ -1096,6 +1104,9 @@ bool tq_choose(int n, int minb, TqChoice* out) {
   g.n = n;
   g.npad = (int)round_up(n, kNB);
   g.lds = smem_stride(g.npad);
+  int npw = 1;
+  if (const char* e = getenv("TSNMF_TSQR_PW")) npw = atoi(e) == 2 ? 2 : 1;
+  g.npw = npw;
   const size_t budget = (minb == 2 ? 113 : 226) * 1024;
   int best = 0;
   for (int b = 16; b <= 32 * kMaxRq; b += 16) {  // multiple of 16: B -= V W' runs row-block pairs
@@ -1104,8 +1115,6 @@ bool tq_choose(int n, int minb, TqChoice* out) {
   }
   if (!best) return false;
   g.brows = best;
-  int npw = 1;
-  if (const char* e = getenv("TSNMF_TSQR_PW")) npw = atoi(e) == 2 ? 2 : 1;
   out->npw = npw;
   out->rq = ((npw == 2 ? best / 2 : best) + 31) / 32;  // rows per lane of each panel warp
   if (out->rq > kMaxRq) return false;
