@@ -124,6 +124,26 @@ def test_tall_shapes_and_tree_edges(oracle, m):
         assert rel_err(f.entries.T @ f.entries, x.T @ x) <= 1e-12
 
 
+@pytest.mark.parametrize("n,m", [(8, 33), (25, 1000), (25, 100_003), (32, 1_000_003), (17, 777_777), (25, 2_500_000)])
+def test_narrow_warp_chain_path(oracle, monkeypatch, n, m):
+    """n <= 32 runs one Householder chain per warp (many leaves, warp-level combine tree with leftover
+    folds, partial 32-row blocks); it must agree with the oracle and with the shared-panel path."""
+    rng = np.random.default_rng(n * 7 + m)
+    x = rng.uniform(-1, 1, (m, n)) * np.logspace(0, -3, n)
+    xd = dev(x)
+    r, l1, sq = dv.tsqr(xd)
+    want = oracle.factor_chunk(x)
+    assert rel_err(r.cpu().numpy(), want) <= R_TOL
+    np.testing.assert_allclose(l1.cpu().numpy(), np.abs(x).sum(0), rtol=1e-12)
+    np.testing.assert_allclose(sq.cpu().numpy(), (x * x).sum(0), rtol=1e-12)
+    monkeypatch.setenv("TSNMF_TSQR_SMALL", "0")
+    r2, _, _ = dv.tsqr(xd)
+    assert rel_err(r2.cpu().numpy(), r.cpu().numpy()) <= R_TOL
+    assert dv.tsqr_plan(n, m)["panel"] == 8
+    monkeypatch.delenv("TSNMF_TSQR_SMALL")
+    assert dv.tsqr_plan(n, m)["panel"] == 1
+
+
 def test_combine_many_factors_tree_order(oracle):
     rng = np.random.default_rng(5)
     rs = [oracle.factor_chunk(rng.standard_normal((60, 20))) for _ in range(13)]
