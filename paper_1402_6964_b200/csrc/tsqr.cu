@@ -1004,6 +1004,7 @@ __device__ __forceinline__ void small_store_r(double* __restrict__ R, int npad, 
 #pragma unroll
     for (int i = 0; i < NC; ++i)
       if (i < npad) R[(int64_t)i * npad + lane] = (i <= lane && lane < n) ? rcol[i] : 0.0;
+    for (int i = NC; i < npad; ++i) R[(int64_t)i * npad + lane] = 0.0;  // NC may be < npad (n < NC <= npad)
   }
 }
 
@@ -1273,10 +1274,15 @@ int small_launch(const double* x, int64_t m, int n, int64_t ldx, int64_t rpw, in
 
 int small_leaf(const double* x, int64_t m, int n, int64_t ldx, int64_t rpw, int nleaves, int npad, double* slots,
                double* stats, cudaStream_t st) {
-  switch (npad) {
-    case 8: return small_launch<8>(x, m, n, ldx, rpw, nleaves, npad, slots, stats, st);
-    case 16: return small_launch<16>(x, m, n, ldx, rpw, nleaves, npad, slots, stats, st);
-    case 24: return small_launch<24>(x, m, n, ldx, rpw, nleaves, npad, slots, stats, st);
+  // register width NC = n rounded up to 4 (the work per column is proportional to NC - j)
+  switch ((n + 3) / 4) {
+    case 1:
+    case 2: return small_launch<8>(x, m, n, ldx, rpw, nleaves, npad, slots, stats, st);
+    case 3: return small_launch<12>(x, m, n, ldx, rpw, nleaves, npad, slots, stats, st);
+    case 4: return small_launch<16>(x, m, n, ldx, rpw, nleaves, npad, slots, stats, st);
+    case 5: return small_launch<20>(x, m, n, ldx, rpw, nleaves, npad, slots, stats, st);
+    case 6: return small_launch<24>(x, m, n, ldx, rpw, nleaves, npad, slots, stats, st);
+    case 7: return small_launch<28>(x, m, n, ldx, rpw, nleaves, npad, slots, stats, st);
     default: return small_launch<32>(x, m, n, ldx, rpw, nleaves, npad, slots, stats, st);
   }
 }
