@@ -207,6 +207,50 @@ def run_reference(args):
 # our arm
 
 
+
+def selection_timing(x, r, n):
+    """XRAY (r picks) + compute_h on the reduced matrix of x's R: device kernels vs the host code (the
+    reference algorithm).  Each side may legitimately fail (e.g. the Lawson-Hanson iteration limit when
+    it cycles at the tolerance); failures are reported, never raised."""
+    import numpy as np
+    import torch
+
+    import paper_1402_6964_b200 as tb
+    from paper_1402_6964_b200 import device as dv, extremes as ex, nonneg as nn
+
+    r_mat, _, _ = dv.tsqr(x)
+    mat = ex.as_matrix(tb.rsvd(tb.TriangularFactor(np.triu(r_mat.cpu().numpy()))))
+
+    def attempt(fn, reps):
+        try:
+            fn()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                out = fn()
+            torch.cuda.synchronize()
+            return (time.perf_counter() - t0) * 1e3 / reps, out, None
+        except Exception as exc:
+            return None, None, f"{type(exc).__name__}: {exc}"
+
+    sel = {"workload": f"XRAY r={r} + compute_h on the {n}x{n} reduced matrix of this pass",
+           "host": "numpy/OpenBLAS Lawson-Hanson (reference algorithm), 1 process"}
+    xd_ms, kd, err = attempt(lambda: ex.xray_order_device(mat, r), 3)
+    sel.update(xray_device_ms=xd_ms, xray_device_error=err)
+    xh_ms, kh, err = attempt(lambda: ex.xray_order(mat, r), 1)
+    sel.update(xray_host_ms=xh_ms, xray_host_error=err)
+    if kd is not None and kh is not None:
+        sel["k_identical"] = list(kd) == list(kh)
+    kset = kd if kd is not None else kh
+    if kset is not None:
+        hd_ms, hd, err = attempt(lambda: nn.solve_columns(mat[:, kset], mat, device=True), 3)
+        sel.update(compute_h_device_ms=hd_ms, compute_h_device_error=err)
+        hh_ms, hh, err = attempt(lambda: nn.solve_columns(mat[:, kset], mat), 1)
+        sel.update(compute_h_host_ms=hh_ms, compute_h_host_error=err)
+        if hd is not None and hh is not None:
+            sel["h_max_abs_diff"] = float(np.abs(hd - hh).max())
+    return {k: v for k, v in sel.items() if v is not None}
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -352,32 +396,10 @@ def main():
 
         # device selection + coefficients (§8f row 1) on this pass's reduced matrix vs the host code
         if rank == 0:
-            import time as _time
-            from paper_1402_6964_b200 import extremes as _ex, nonneg as _nn
-
-            r_mat, _, _ = dv.tsqr(x)
-            red = tb.rsvd(tb.TriangularFactor(np.triu(r_mat.cpu().numpy())))
-            mat = _ex.as_matrix(red)
-
-            def wall(fn, reps):
-                fn()
-                torch.cuda.synchronize()
-                t0 = _time.perf_counter()
-                for _ in range(reps):
-                    out = fn()
-                torch.cuda.synchronize()
-                return (_time.perf_counter() - t0) * 1e3 / reps, out
-
-            xd_ms, kd = wall(lambda: _ex.xray_order_device(mat, spec.r), 3)
-            hd_ms, hd = wall(lambda: _nn.solve_columns(mat[:, kd], mat, device=True), 3)
-            xh_ms, kh = wall(lambda: _ex.xray_order(mat, spec.r), 1)
-            hh_ms, hh = wall(lambda: _nn.solve_columns(mat[:, kh], mat), 1)
-            line["selection"] = {"workload": f"XRAY r={spec.r} + compute_h on the {n}x{n} reduced matrix of this pass",
-                                 "xray_device_ms": xd_ms, "xray_host_ms": xh_ms,
-                                 "compute_h_device_ms": hd_ms, "compute_h_host_ms": hh_ms,
-                                 "k_identical": list(kd) == list(kh),
-                                 "h_max_abs_diff": float(np.abs(hd - hh).max()) if list(kd) == list(kh) else None,
-                                 "host": "numpy/OpenBLAS Lawson-Hanson (reference algorithm), 1 process"}
+            try:
+                line["selection"] = selection_timing(x, spec.r, n)
+            except Exception as exc:  # never lose the headline line to an optional extra
+                line["selection"] = {"error": f"{type(exc).__name__}: {exc}"}
 
     # end to end through the public API from pinned host buffers (H2D inside the timed region)
     if not args.no_e2e:
@@ -424,8 +446,11 @@ def main():
         assert res.rows == hi - lo
 
     if rank == 0 and world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_reference(args.config, n, args.cpu_seconds)
-        line["cpu_baseline"].pop("seconds", None)
+        try:
+            line["cpu_baseline"] = cpu_reference(args.config, n, args.cpu_seconds)
+            line["cpu_baseline"].pop("seconds", None)
+        except Exception as exc:
+            line["cpu_baseline"] = {"error": f"{type(exc).__name__}: {exc}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
