@@ -9,20 +9,18 @@
 // Leaf: each CTA owns a contiguous row range and an R slot (npad x npad, row-major, L2-resident in the
 // caller's workspace).  It streams row blocks B (brows x npad) into shared memory and folds each block
 // into R with a structured blocked Householder QR of [R; B]: the reflector for column j is
-// u = [e_j; v] (R part is a unit vector), so only R row j and the block are touched.  Panels of NB
-// columns are factored cooperatively (warp shuffles + one CTA barrier per column); the trailing update
-// uses the compact-WY form  W = R_p + V^T B,  W <- T^T W,  R_p -= W,  B -= V W  on FP64 tensor cores
-// (mma.sync m8n8k4 f64 = DMMA).  Leaves are then combined in the reference TreeReducer order (perfect
+// u = [e_j; v] (R part is a unit vector), so only R row j and the block are touched.  Panels of NB = 8
+// columns are factored by one register-resident panel warp with lazy trailing updates (no CTA barrier
+// per column); the next panel's columns get the lookahead update from the panel warp + helper pair and
+// the rest of the trailing matrix the compact-WY update  W = R_p + V^T B,  W <- T^T W,  R_p -= W,
+// B -= V W  by six GEMM warps on FP64 tensor cores (mma.sync m8n8k4 f64 = DMMA), overlapped with the
+// next panel.  Narrow matrices (n <= 32) use a warp-per-chain leaf instead (tsqr_small_leaf_kernel).  Leaves are then combined in the reference TreeReducer order (perfect
 // binary levels over the leaf index, then a fold of the leftover subtrees), each combine being the same
 // structured QR with the second factor's rows as data (triangular: panels left of the block are skipped).
 #include "common.cuh"
 #include "internal.h"
 
 namespace tsnmf {
-
-#ifndef TSNMF_HELPER_LOOKAHEAD
-#define TSNMF_HELPER_LOOKAHEAD 1
-#endif
 
 constexpr int kTqThreads = 256;
 constexpr int kTqWarps = kTqThreads / 32;
@@ -33,22 +31,17 @@ struct TqGeom {
   int n;      // data columns
   int npad;   // padded columns (multiple of 8); R slots are npad x npad
   int lds;    // shared-memory row stride of the block (% 16 == 8)
-  int brows;  // rows per block (multiple of 8, <= 64 * kMaxRq)
-  int npw;    // panel warps (1: lean layout — one reduction scratch, pair-lookahead partials only)
+  int brows;  // rows per block (multiple of 8, <= 32 * kMaxRq)
 };
 
 struct TqLayout {
   // offsets in doubles from the dynamic smem base
   __host__ __device__ static int rd(const TqGeom& g) { return g.brows * g.lds; }            // 2 x 8x8 R diag blocks
   __host__ __device__ static int tm(const TqGeom& g) { return rd(g) + 2 * kNB * kNB; }      // 2 x 8x8 T
-  __host__ __device__ static int red(const TqGeom& g) { return tm(g) + 2 * kNB * kNB; }    // npw x 32 x 9 partials
-  __host__ __device__ static int xch(const TqGeom& g) { return red(g) + g.npw * 32 * 9; }  // 2 x 16 exchange
-  __host__ __device__ static int wsc(const TqGeom& g) { return xch(g) + 32; }                // per-warp 8x8 scratch
+  __host__ __device__ static int red(const TqGeom& g) { return tm(g) + 2 * kNB * kNB; }    // 32 x 9 partials
+  __host__ __device__ static int wsc(const TqGeom& g) { return red(g) + 32 * 9; }           // per-warp 8x8 scratch
   __host__ __device__ static int wpart(const TqGeom& g) { return wsc(g) + kTqWarps * kNB * 8; }  // partial W tiles
-  // 6 partial W + W' for the cooperative lookahead (NPW == 2), 2 for the pair lookahead (NPW == 1)
-  __host__ __device__ static int total(const TqGeom& g) {
-    return wpart(g) + ((g.npw == 2 || TSNMF_HELPER_LOOKAHEAD == 0) ? 7 : 2) * 64;
-  }
+  __host__ __device__ static int total(const TqGeom& g) { return wpart(g) + 2 * 64; }  // pair-lookahead partials
   static size_t bytes(const TqGeom& g) { return sizeof(double) * (size_t)total(g); }
 };
 
@@ -63,7 +56,7 @@ __device__ __forceinline__ int swz(int row) { return (row & 2) << 1; }
 // FP64 chain without DMMA traffic; warps 1,2,3,5,6,7 = GEMM warps (GEMM warp 0 also stages R rows).
 constexpr int kBarColsReady = 1;  // next panel's columns updated + its R rows staged  (GEMM, helper -> panel)
 constexpr int kBarPanelDone = 2;  // V, T of the current panel published               (panel -> GEMM, helper)
-constexpr int kBarGemm = 3;       // among the 6 GEMM warps (cooperative lookahead update)
+constexpr int kBarPanelPair = 4;  // panel warp + helper (pair lookahead partials)
 constexpr int kGemmWarps = 6;
 __device__ __forceinline__ void named_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
@@ -96,25 +89,6 @@ __device__ long long g_trace[8][64 * 64];
   } while (0)
 #endif
 
-// Panel factorization of columns [j0, j0 + 8) by the TWO panel warps (warps 0 and 4, both on SMSP 0,
-// which carries no DMMA traffic).  Panel warp h holds block rows [h*half, (h+1)*half) in registers,
-// row = h*half + lane + 32 q.  Per column: dot products of the current column with all 8 panel
-// columns (its norm, the trailing dots for the update, the V^T v dots for T) are reduced within each
-// warp by a transposed shared-memory sum, the two warp totals are exchanged through shared memory with
-// one 64-thread named barrier and added in fixed order (both warps get bit-identical totals, so they
-// compute identical reflectors).  Reflector (dlarfg convention): beta = -sign(alpha) ||(alpha, x)||,
-// tau = (beta - alpha)/beta, v = x/(alpha - beta).  T (upper triangular, dlarft forward columnwise) is
-// built incrementally off the critical path; R row entries are kept in registers (lane c owns column
-// c) and stored once per panel.  Rd: the 8x8 diagonal block of R for this panel, staged in shared memory.
-constexpr int kBarPanelPair = 4;
-#ifndef TSNMF_LAZY_PANEL
-#define TSNMF_LAZY_PANEL 1
-#endif
-constexpr bool kLazyPanel = TSNMF_LAZY_PANEL != 0;
-#ifndef TSNMF_HELPER_LOOKAHEAD
-#define TSNMF_HELPER_LOOKAHEAD 1
-#endif
-constexpr bool kHelperLookahead = TSNMF_HELPER_LOOKAHEAD != 0;
 #ifndef TSNMF_PAIR_LOOKAHEAD
 #define TSNMF_PAIR_LOOKAHEAD 1
 #endif
@@ -141,114 +115,14 @@ __device__ __forceinline__ double fast_rcp(double a) {
   return y;
 }
 
-template <int RQ, int NPW>
-__device__ __forceinline__ void panel_factor(double* __restrict__ Bs, int lds, int brows, int j0,
-                                             double* __restrict__ R, int npad, const double* __restrict__ Rd,
-                                             double* __restrict__ Tm, double* __restrict__ red,
-                                             double* __restrict__ xch, int h, int lane, int tq_p) {
-  const int half = NPW == 2 ? (brows + 1) / 2 : brows;
-  const int row0 = h * half;
-  const int rows_mine = h == 0 ? half : brows - half;
-  const int sw = swz(row0 + lane);  // half is a multiple of 4 -> (row & 2) = (lane & 2)
-  double x[RQ][kNB];
-#pragma unroll
-  for (int q = 0; q < RQ; ++q) {
-    const int rl = lane + 32 * q;
-    const double* rp = Bs + (row0 + rl) * lds + j0;
-#pragma unroll
-    for (int c = 0; c < kNB; c += 2) {  // 16-byte accesses: swizzle keeps (c, c+1) pairs adjacent
-      double2 v = make_double2(0.0, 0.0);
-      if (rl < rows_mine) v = *reinterpret_cast<const double2*>(rp + (c ^ sw));
-      x[q][c] = v.x;
-      x[q][c + 1] = v.y;
-    }
-  }
-  double trow[kNB], rmine[kNB];
-#pragma unroll
-  for (int c = 0; c < kNB; ++c) trow[c] = rmine[c] = 0.0;
-  double* redw = red + h * (32 * 9);
-  const int rc = lane & 7, rq = lane >> 3;  // reduction role: column, quarter of the warp
-#pragma unroll
-  for (int jj = 0; jj < kNB; ++jj) {
-    TQ_TRACE(10 + jj);
-#pragma unroll
-    for (int c = 0; c < kNB; ++c) {
-      double acc = 0.0;
-#pragma unroll
-      for (int q = 0; q < RQ; ++q) acc = fma(x[q][jj], x[q][c], acc);
-      redw[lane * 9 + c] = acc;
-    }
-    __syncwarp();
-    const double s0 = redw[(rq * 8 + 0) * 9 + rc] + redw[(rq * 8 + 1) * 9 + rc];
-    const double s1 = redw[(rq * 8 + 2) * 9 + rc] + redw[(rq * 8 + 3) * 9 + rc];
-    const double s2 = redw[(rq * 8 + 4) * 9 + rc] + redw[(rq * 8 + 5) * 9 + rc];
-    const double s3 = redw[(rq * 8 + 6) * 9 + rc] + redw[(rq * 8 + 7) * 9 + rc];
-    double tot = (s0 + s1) + (s2 + s3);
-    tot += __shfl_xor_sync(0xffffffffu, tot, 8);
-    tot += __shfl_xor_sync(0xffffffffu, tot, 16);
-    double d[kNB];
-    if (NPW == 2) {
-      double* xw = xch + (jj & 1) * 16;  // double-buffered exchange slots
-      if (lane < 8) xw[h * 8 + lane] = tot;
-      named_sync(kBarPanelPair, 64);
-#pragma unroll
-      for (int c = 0; c < kNB; ++c) d[c] = xw[c] + xw[8 + c];
-    } else {
-#pragma unroll
-      for (int c = 0; c < kNB; ++c) d[c] = __shfl_sync(0xffffffffu, tot, c);
-    }
-    TQ_TRACE(30 + jj);
-    const double alpha = Rd[jj * kNB + jj];
-    double tau = 0.0, scale = 0.0, beta = alpha;
-    if (d[jj] > 0.0) {
-      // inv = 1/||(alpha, x)||;  tau = (beta - alpha)/beta = 1 + |alpha| inv;  scale = sign(alpha)/(|alpha| + nrm)
-      const double ss = fma(alpha, alpha, d[jj]);
-      const double inv = fast_rsqrt(ss);
-      const double nrm = ss * inv;
-      beta = -copysign(nrm, alpha);
-      tau = fma(fabs(alpha), inv, 1.0);
-      scale = copysign(fast_rcp(fabs(alpha) + nrm), alpha);
-    }
-#pragma unroll
-    for (int c = jj + 1; c < kNB; ++c) {
-      const double rjc = Rd[jj * kNB + c];
-      const double tw = tau * fma(scale, d[c], rjc);
-      const double f = tw * scale;
-#pragma unroll
-      for (int q = 0; q < RQ; ++q) x[q][c] = fma(-f, x[q][jj], x[q][c]);
-      if (lane == c) rmine[jj] = rjc - tw;
-    }
-#pragma unroll
-    for (int q = 0; q < RQ; ++q) x[q][jj] *= scale;
-    if (lane == jj) rmine[jj] = beta;
-    {  // T[r][jj] = -tau_jj * sum_{q=r}^{jj-1} T[r][q] (v_q^T v_jj),  v_q^T v_jj = scale * d[q]
-      double acc = 0.0;
-#pragma unroll
-      for (int q = 0; q < jj; ++q) acc = fma(trow[q], d[q], acc);
-      trow[jj] = (lane == jj) ? tau : (lane < jj ? -tau * scale * acc : 0.0);
-    }
-    __syncwarp();  // redw reuse
-  }
-#pragma unroll
-  for (int q = 0; q < RQ; ++q) {
-    const int rl = lane + 32 * q;
-    if (rl < rows_mine) {
-      double* rp = Bs + (row0 + rl) * lds + j0;
-#pragma unroll
-      for (int c = 0; c < kNB; c += 2) *reinterpret_cast<double2*>(rp + (c ^ sw)) = make_double2(x[q][c], x[q][c + 1]);
-    }
-  }
-  if (h == 0 && lane < kNB) {
-    double* Rcol = R + (int64_t)j0 * npad + j0 + lane;  // lane c writes R(j0 + jj, j0 + c), jj <= c
-#pragma unroll
-    for (int jj = 0; jj < kNB; ++jj)
-      if (jj <= lane) Rcol[(int64_t)jj * npad] = rmine[jj];
-#pragma unroll
-    for (int c = 0; c < kNB; ++c) Tm[lane * kNB + c] = trow[c];
-  }
-}
-
-// Single-warp panel with LAZY trailing updates (the NPW == 1 path).  Step s (column j0 + s):
+// Panel factorization of columns [j0, j0 + 8) by ONE warp (warp 0, on SMSP 0, which carries no trailing
+// DMMA traffic), block rows in registers (row = lane + 32 q).  Reflector (dlarfg convention):
+// beta = -sign(alpha) ||(alpha, x)||, tau = (beta - alpha)/beta, v = x/(alpha - beta); T (upper
+// triangular, dlarft forward columnwise) is built incrementally off the critical path; R row entries are
+// kept in registers (lane c owns column c) and stored once per panel; Rd is the 8x8 diagonal block of R
+// for this panel, staged in shared memory.  Per column, the dot products of the pivot with the 8 panel
+// columns are reduced by a transposed shared-memory sum + 2 butterfly shuffles.
+// LAZY trailing updates.  Step s (column j0 + s):
 //   * only the next pivot column is updated eagerly:  x_s -= f_s * u_{s-1}   (u = previous pivot, unscaled)
 //   * dot products P_c = x_s . x_c use the trailing columns BEFORE step s-1's update, then are corrected
 //     d_c = P_c - f_c * P_{s-1}  (x_c' = x_c - f_c u_{s-1});  P_{s-1} = x_s . u_{s-1} also gives the T dot
@@ -651,76 +525,18 @@ __device__ __forceinline__ void lookahead_pair(double* __restrict__ Bs, int lds,
   }
 }
 
-// Cooperative lookahead: the 6 GEMM warps apply panel (j0)'s reflector to the single column block cb
-// (the next panel's columns).  GEMM1 is split over rows (k-step i/4 = gi mod 6) into 6 partial W tiles
-// summed in fixed order by GEMM warp 0, which also forms W' = T^T W and updates R; then each warp
-// updates its row blocks (rb = gi mod 6).  Two barriers among the GEMM warps only.
-__device__ __forceinline__ void lookahead_cb(double* __restrict__ Bs, int lds, int brows, int j0,
-                                             double* __restrict__ R, int npad, const double* __restrict__ Tm,
-                                             double* __restrict__ Wpart, int cb, int gi, int lane) {
-  const int frag_col = (lane >> 2) ^ ((lane & 2) << 1);
-  const int vsw = ((lane >> 2) & 2) << 1;
-  double* rtile = R + (int64_t)(j0 + (lane >> 2)) * npad + 8 * cb + 2 * (lane & 3);
-  double2 rinit = make_double2(0.0, 0.0);
-  if (gi == 0) rinit = *reinterpret_cast<const double2*>(rtile);  // early: latency hidden by the k-loop
-  double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
-  const double* slab = Bs + (lane & 3) * lds + frag_col;
-  int it = 0;
-  for (int i = 4 * gi; i < brows; i += 4 * kGemmWarps, ++it) {
-    const double* r = slab + i * lds;
-    if (it & 1) dmma(e0, e1, r[j0], r[8 * cb]);
-    else dmma(c0, c1, r[j0], r[8 * cb]);
-  }
-  const int ci = (lane >> 2) * 8 + 2 * (lane & 3);
-  Wpart[gi * 64 + ci] = c0 + e0;
-  Wpart[gi * 64 + ci + 1] = c1 + e1;
-  named_sync(kBarGemm, 32 * kGemmWarps);
-  double* Wsh = Wpart + 6 * 64;
-  if (gi == 0) {
-    double w0 = rinit.x, w1 = rinit.y;
-#pragma unroll
-    for (int g = 0; g < kGemmWarps; ++g) {
-      w0 += Wpart[g * 64 + ci];
-      w1 += Wpart[g * 64 + ci + 1];
-    }
-    __syncwarp();
-    Wsh[ci] = w0;  // W (natural row-major 8x8)
-    Wsh[ci + 1] = w1;
-    __syncwarp();
-    double v0 = 0.0, v1 = 0.0;
-#pragma unroll
-    for (int k0 = 0; k0 < 8; k0 += 4)
-      dmma(v0, v1, Tm[(k0 + (lane & 3)) * kNB + (lane >> 2)], Wsh[(k0 + (lane & 3)) * 8 + (lane >> 2)]);
-    *reinterpret_cast<double2*>(rtile) = make_double2(rinit.x - v0, rinit.y - v1);
-    __syncwarp();
-    Wsh[ci] = v0;  // W'
-    Wsh[ci + 1] = v1;
-  }
-  named_sync(kBarGemm, 32 * kGemmWarps);
-  const double wb0 = -Wsh[(lane & 3) * 8 + (lane >> 2)];
-  const double wb1 = -Wsh[(4 + (lane & 3)) * 8 + (lane >> 2)];
-  for (int rb = gi; rb < brows / 8; rb += kGemmWarps) {
-    double* rowp = Bs + (8 * rb + (lane >> 2)) * lds;
-    const double a0 = rowp[j0 + ((lane & 3) ^ vsw)], a1 = rowp[j0 + ((4 + (lane & 3)) ^ vsw)];
-    double2* cp = reinterpret_cast<double2*>(rowp + 8 * cb + ((2 * (lane & 3)) ^ vsw));
-    double2 cv = *cp;
-    dmma(cv.x, cv.y, a0, wb0);
-    dmma(cv.x, cv.y, a1, wb1);
-    *cp = cv;
-  }
-}
-
 // Fold `nrows` data rows (row-major, stride ldsrc, `ncols` real columns) into the R slot `R`.
 // triangular: data row i is zero left of column i (the data is another R factor).
 //
-// Lookahead schedule per panel p (warp 0 = panel warp on SMSP 0, warp 4 = helper, 6 GEMM warps):
-//   panel warp : wait ColsReady(p) -> factor panel p -> arrive PanelDone(p)
-//   helper     : wait PanelDone(p) -> stage R rows of panel p+1 -> arrive ColsReady(p+1)
-//   GEMM warps : wait PanelDone(p) -> cooperatively update column block p+1 -> arrive ColsReady(p+1)
-//                -> update column blocks p+2.. with panel p
+// Lookahead schedule per panel p (warp 0 = panel warp and warp 4 = helper, both on SMSP 0; warps
+// 1,2,3,5,6,7 = GEMM warps on SMSPs 1..3):
+//   panel warp : wait ColsReady(p) -> factor panel p -> arrive PanelDone(p) -> its half of the lookahead
+//   helper     : wait PanelDone(p) -> stage R diag of panel p+1 -> its half of the lookahead (update of
+//                column block p+1 with panel p, lookahead_pair) -> arrive ColsReady(p+1)
+//   GEMM warps : wait PanelDone(p) -> arrive ColsReady(p+1) -> update column blocks p+2.. with panel p
 // so panel p+1 is factored while the trailing update of panel p runs.  V_p lives in the block's
 // panel-p columns (never touched again this block); T and the staged R rows are double-buffered.
-template <int RQ, int NPW>
+template <int RQ>
 __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src, int64_t nrows, int64_t ldsrc,
                           int ncols, const TqGeom g, bool triangular, bool init_zero,
                           double* __restrict__ stats_out, double* smem) {
@@ -734,7 +550,6 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
   double* red = smem + L::red(g);
   double* Wsc = smem + L::wsc(g) + warp * kNB * 8;
   double* Wpart = smem + L::wpart(g);
-  double* xch = smem + L::xch(g);
   const int npanels = npad / kNB, ncb = npad / 8;
   const bool vec16 = ((ldsrc & 1) == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
 
@@ -775,38 +590,30 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
       const double* Tmc = Tm + buf * kNB * kNB;
       const bool more = p + 1 < npanels;
       const int tq_p = (r0 == 0 && p < 64) ? p : -1;
-      if (warp == 0 || (NPW == 2 && warp == 4)) {
+      if (warp == 0) {
         if (p > p0) named_sync(kBarColsReady, kTqThreads);
         TQ_RESOLVE(Rdg);
         TQ_TRACE(1);
-        if (NPW == 1 && kLazyPanel)
-          panel_factor_lazy<RQ>(Bs, lds, brows, j0, R, npad, Rdc, Tm + buf * kNB * kNB, red, lane, tq_p);
-        else
-          panel_factor<RQ, NPW>(Bs, lds, brows, j0, R, npad, Rdc, Tm + buf * kNB * kNB, red, xch, warp >> 2, lane,
-                                tq_p);
+        panel_factor_lazy<RQ>(Bs, lds, brows, j0, R, npad, Rdc, Tm + buf * kNB * kNB, red, lane, tq_p);
         TQ_TRACE(2);
         named_arrive(kBarPanelDone, kTqThreads);
-        if (NPW == 1 && kHelperLookahead && kPairLookahead && more) {
+        if (kPairLookahead && more) {
           __syncwarp();  // the warp's own V / T stores are visible to all its lanes
           lookahead_pair(Bs, lds, brows, j0, R, npad, Tmc, Wpart, Wsc, p + 1, 0, lane);
         }
       } else if (warp == 4) {
-        // NPW == 1: helper on SMSP 0.  While the panel warp waits for ColsReady it is idle, so the helper
-        // does the lookahead alone (update of the next panel's column block with panel p) plus the R diag
-        // staging; it starts the moment the panel is published instead of after the GEMM warps' trailing
-        // work, and its DMMAs never overlap the panel's FP64 chain on this SMSP.
+        // helper on SMSP 0: the lookahead starts the moment the panel is published (not after the GEMM
+        // warps' trailing work) and its DMMAs never overlap the panel's FP64 chain on this SMSP
         named_sync(kBarPanelDone, kTqThreads);
         TQ_RESOLVE(Rdg);
         if (more) {
           TQ_TRACE(3);
           stage_rdiag(Rdg + (buf ^ 1) * kNB * kNB, R, npad, j0 + kNB, lane);
           cp_async_commit();
-          if (kHelperLookahead) {
-            if (kPairLookahead)
-              lookahead_pair(Bs, lds, brows, j0, R, npad, Tmc, Wpart, Wsc, p + 1, 1, lane);
-            else
-              lookahead_single(Bs, lds, brows, j0, R, npad, Tmc, Wsc, p + 1, lane);
-          }
+          if (kPairLookahead)
+            lookahead_pair(Bs, lds, brows, j0, R, npad, Tmc, Wpart, Wsc, p + 1, 1, lane);
+          else
+            lookahead_single(Bs, lds, brows, j0, R, npad, Tmc, Wsc, p + 1, lane);
           cp_async_wait<0>();
           __syncwarp();
           TQ_TRACE(4);
@@ -816,23 +623,7 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
         const int gi = gemm_index(warp);
         named_sync(kBarPanelDone, kTqThreads);
         TQ_RESOLVE(Rdg);
-        if (more) {
-          if (NPW == 2 || !kHelperLookahead) {
-            TQ_TRACE(3);
-            const bool stager = NPW == 2 && gi == 0;  // with two panel warps, GEMM warp 0 stages the R diag block
-            if (stager) {
-              stage_rdiag(Rdg + (buf ^ 1) * kNB * kNB, R, npad, j0 + kNB, lane);
-              cp_async_commit();
-            }
-            lookahead_cb(Bs, lds, brows, j0, R, npad, Tmc, Wpart, p + 1, gi, lane);
-            if (stager) {
-              cp_async_wait<0>();
-              __syncwarp();
-            }
-            TQ_TRACE(4);
-          }
-          named_arrive(kBarColsReady, kTqThreads);
-        }
+        if (more) named_arrive(kBarColsReady, kTqThreads);
         // trailing column blocks p+2 .. ncb-1, round-robin over the GEMM warps in groups of G
         for (int base = p + 2 + gi; base < ncb; base += kGemmWarps * G) {
           int cnt_g = 0;
@@ -866,7 +657,7 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
   }
 }
 
-template <int RQ, int NPW, int MINB>
+template <int RQ, int MINB>
 __global__ void __launch_bounds__(kTqThreads, MINB)
     tsqr_leaf_kernel(const double* __restrict__ x, int64_t m, int64_t ldx, int64_t rows_per_cta, TqGeom g,
                      double* __restrict__ slots, double* __restrict__ stats) {
@@ -875,12 +666,12 @@ __global__ void __launch_bounds__(kTqThreads, MINB)
   const int64_t cnt = max64(0, min64(rows_per_cta, m - r0));
   double* R = slots + (int64_t)blockIdx.x * g.npad * g.npad;
   double* st = stats ? stats + (int64_t)blockIdx.x * 2 * g.npad : nullptr;
-  tsqr_fold<RQ, NPW>(R, x + r0 * ldx, cnt, ldx, g.n, g, false, true, st, smem);
+  tsqr_fold<RQ>(R, x + r0 * ldx, cnt, ldx, g.n, g, false, true, st, smem);
 }
 
 // One level of the binary-counter tree: slot[q*2^L] = qr([slot[q*2^L]; slot[q*2^L + 2^(L-1)]]),
 // or (fold) slot[dst] = qr([slot[dst]; slot[src]]).
-template <int RQ, int NPW, int MINB>
+template <int RQ, int MINB>
 __global__ void __launch_bounds__(kTqThreads, MINB)
     tsqr_combine_kernel(double* __restrict__ slots, int64_t span, int64_t half, int64_t fold_dst, int64_t fold_src,
                         TqGeom g) {
@@ -894,7 +685,7 @@ __global__ void __launch_bounds__(kTqThreads, MINB)
     dst = fold_dst;
     srcs = fold_src;
   }
-  tsqr_fold<RQ, NPW>(slots + dst * ss, slots + srcs * ss, g.npad, g.npad, g.npad, g, true, false, nullptr, smem);
+  tsqr_fold<RQ>(slots + dst * ss, slots + srcs * ss, g.npad, g.npad, g.npad, g, true, false, nullptr, smem);
 }
 
 // ---------------------------------------------------------------------------
@@ -1093,8 +884,7 @@ __global__ void tsqr_pad_kernel(const double* __restrict__ rs, int n, int npad, 
 namespace {
 
 struct TqChoice {
-  int rq;
-  int npw;  // panel warps (1 or 2)
+  int rq;    // block rows per lane of the panel warp
   int minb;
   TqGeom g;
   size_t smem;
@@ -1105,9 +895,6 @@ bool tq_choose(int n, int minb, TqChoice* out) {
   g.n = n;
   g.npad = (int)round_up(n, kNB);
   g.lds = smem_stride(g.npad);
-  int npw = 1;
-  if (const char* e = getenv("TSNMF_TSQR_PW")) npw = atoi(e) == 2 ? 2 : 1;
-  g.npw = npw;
   const size_t budget = (minb == 2 ? 113 : 226) * 1024;
   int best = 0;
   for (int b = 16; b <= 32 * kMaxRq; b += 16) {  // multiple of 16: B -= V W' runs row-block pairs
@@ -1116,8 +903,7 @@ bool tq_choose(int n, int minb, TqChoice* out) {
   }
   if (!best) return false;
   g.brows = best;
-  out->npw = npw;
-  out->rq = ((npw == 2 ? best / 2 : best) + 31) / 32;  // rows per lane of each panel warp
+  out->rq = (best + 31) / 32;
   if (out->rq > kMaxRq) return false;
   out->minb = minb;
   out->g = g;
@@ -1136,20 +922,20 @@ bool tq_config(int n, TqChoice* out) {
   return tq_choose(n, 1, out);
 }
 
-template <int RQ, int NPW, int MINB>
+template <int RQ, int MINB>
 int tq_launch_all(const TqChoice& ch, const double* x, int64_t m, int64_t ldx, double* slots, double* stats,
                   int nleaves, int64_t rows_per_cta, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
-    TSNMF_CUDA_CHECK(cudaFuncSetAttribute(tsqr_leaf_kernel<RQ, NPW, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    TSNMF_CUDA_CHECK(cudaFuncSetAttribute(tsqr_leaf_kernel<RQ, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           232448));
-    TSNMF_CUDA_CHECK(cudaFuncSetAttribute(tsqr_combine_kernel<RQ, NPW, MINB>,
+    TSNMF_CUDA_CHECK(cudaFuncSetAttribute(tsqr_combine_kernel<RQ, MINB>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
     attr_set = true;
   }
   if (x) {
     prof_mark(kProfTsqrLeaf, true, st);
-    tsqr_leaf_kernel<RQ, NPW, MINB><<<nleaves, kTqThreads, ch.smem, st>>>(x, m, ldx, rows_per_cta, ch.g, slots, stats);
+    tsqr_leaf_kernel<RQ, MINB><<<nleaves, kTqThreads, ch.smem, st>>>(x, m, ldx, rows_per_cta, ch.g, slots, stats);
     TSNMF_LAUNCH_CHECK();
     prof_mark(kProfTsqrLeaf, false, st);
   }
@@ -1157,7 +943,7 @@ int tq_launch_all(const TqChoice& ch, const double* x, int64_t m, int64_t ldx, d
   // binary-counter tree (tsqr.py:213-230): perfect levels, then fold leftover subtrees low -> high
   for (int64_t span = 2; span <= nleaves; span *= 2) {
     const int64_t q = nleaves / span;
-    tsqr_combine_kernel<RQ, NPW, MINB><<<(unsigned)q, kTqThreads, ch.smem, st>>>(slots, span, span / 2, 0, 0, ch.g);
+    tsqr_combine_kernel<RQ, MINB><<<(unsigned)q, kTqThreads, ch.smem, st>>>(slots, span, span / 2, 0, 0, ch.g);
     TSNMF_LAUNCH_CHECK();
   }
   int64_t offs[64];
@@ -1169,32 +955,28 @@ int tq_launch_all(const TqChoice& ch, const double* x, int64_t m, int64_t ldx, d
       o += (1LL << b);
     }
   for (int t = nsub - 2; t >= 0; --t) {
-    tsqr_combine_kernel<RQ, NPW, MINB><<<1, kTqThreads, ch.smem, st>>>(slots, 0, 0, offs[t], offs[t + 1], ch.g);
+    tsqr_combine_kernel<RQ, MINB><<<1, kTqThreads, ch.smem, st>>>(slots, 0, 0, offs[t], offs[t + 1], ch.g);
     TSNMF_LAUNCH_CHECK();
   }
   prof_mark(kProfTsqrTree, false, st);
   return kOk;
 }
 
-template <int NPW, int MINB>
+template <int MINB>
 int tq_dispatch_rq(const TqChoice& ch, const double* x, int64_t m, int64_t ldx, double* slots, double* stats,
                    int nleaves, int64_t rows_per_cta, cudaStream_t st) {
   switch (ch.rq) {
-    case 1: return tq_launch_all<1, NPW, MINB>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
-    case 2: return tq_launch_all<2, NPW, MINB>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
-    case 3: return tq_launch_all<3, NPW, MINB>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
-    default: return tq_launch_all<4, NPW, MINB>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
+    case 1: return tq_launch_all<1, MINB>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
+    case 2: return tq_launch_all<2, MINB>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
+    case 3: return tq_launch_all<3, MINB>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
+    default: return tq_launch_all<4, MINB>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
   }
 }
 
 int tq_dispatch(const TqChoice& ch, const double* x, int64_t m, int64_t ldx, double* slots, double* stats,
                 int nleaves, int64_t rows_per_cta, cudaStream_t st) {
-  if (ch.npw == 2) {
-    if (ch.minb == 2) return tq_dispatch_rq<2, 2>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
-    return tq_dispatch_rq<2, 1>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
-  }
-  if (ch.minb == 2) return tq_dispatch_rq<1, 2>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
-  return tq_dispatch_rq<1, 1>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
+  if (ch.minb == 2) return tq_dispatch_rq<2>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
+  return tq_dispatch_rq<1>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
 }
 
 int device_sms() {
