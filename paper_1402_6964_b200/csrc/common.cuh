@@ -177,8 +177,6 @@ __host__ __device__ __forceinline__ int smem_stride(int cols) {
   return s;
 }
 
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-
 // cp.async helpers (LDGSTS): global -> shared without staging through registers.
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -251,11 +249,6 @@ __device__ __forceinline__ void stage_rows_swz(double* __restrict__ dst, int lds
                                                int64_t ldsrc, int nrows, int ncols, int rows_total,
                                                int cols_total, bool vec16) {
   stage_rows_impl<true>(dst, lds, src, ldsrc, nrows, ncols, rows_total, cols_total, vec16);
-}
-__device__ __forceinline__ void stage_rows(double* __restrict__ dst, int lds, const double* __restrict__ src,
-                                           int64_t ldsrc, int nrows, int ncols, int rows_total,
-                                           int cols_total, bool vec16) {
-  stage_rows_impl<false>(dst, lds, src, ldsrc, nrows, ncols, rows_total, cols_total, vec16);
 }
 
 }  // namespace tsnmf
