@@ -98,41 +98,25 @@ constexpr bool kPairLookahead = TSNMF_PAIR_LOOKAHEAD != 0;  // panel warp joins 
 // correct bits: ~23 -> ~46 -> full), accurate to ~1 ulp; outside [2^-900, 2^900] (where the .ftz
 // approximation would flush) the IEEE library versions are used.  a > 0 here.
 __device__ __forceinline__ double fast_rsqrt(double a) {
-  if (!(a > 0x1p-900 && a < 0x1p+900)) return rsqrt(a);  // denormal / extreme range: IEEE path
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
   const double h = 0.5 * a;
   y = y * fma(-h * y, y, 1.5);
   y = y * fma(-h * y, y, 1.5);
+  // the range test runs beside the Newton chain (not in front of it); the branch is almost never taken
+  if (!(a > 0x1p-900 && a < 0x1p+900)) y = rsqrt(a);  // denormal / extreme range: IEEE path
   return y;
 }
 __device__ __forceinline__ double fast_rcp(double a) {
-  if (!(a > 0x1p-900 && a < 0x1p+900)) return __drcp_rn(a);
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
   y = y * fma(-a, y, 2.0);
   y = y * fma(-a, y, 2.0);
+  if (!(a > 0x1p-900 && a < 0x1p+900)) y = __drcp_rn(a);
   return y;
 }
 
-// Panel factorization of columns [j0, j0 + 8) by ONE warp (warp 0, on SMSP 0, which carries no trailing
-// DMMA traffic), block rows in registers (row = lane + 32 q).  Reflector (dlarfg convention):
-// beta = -sign(alpha) ||(alpha, x)||, tau = (beta - alpha)/beta, v = x/(alpha - beta); T (upper
-// triangular, dlarft forward columnwise) is built incrementally off the critical path; R row entries are
-// kept in registers (lane c owns column c) and stored once per panel; Rd is the 8x8 diagonal block of R
-// for this panel, staged in shared memory.  Per column, the dot products of the pivot with the 8 panel
-// columns are reduced by a transposed shared-memory sum + 2 butterfly shuffles.
-// LAZY trailing updates.  Step s (column j0 + s):
-//   * only the next pivot column is updated eagerly:  x_s -= f_s * u_{s-1}   (u = previous pivot, unscaled)
-//   * dot products P_c = x_s . x_c use the trailing columns BEFORE step s-1's update, then are corrected
-//     d_c = P_c - f_c * P_{s-1}  (x_c' = x_c - f_c u_{s-1});  P_{s-1} = x_s . u_{s-1} also gives the T dot
-//     v_{s-1}^T x_s = scale_{s-1} P_{s-1};
-//   * the pending trailing updates and the scaling u_{s-1} -> v_{s-1} run off the critical path, after the
-//     dots have been issued.
-// The critical path per column is: scalars -> one column update -> dots -> warp reduction -> corrections.
-// Rounding: the corrected dots carry errors O(eps |x_s| |x_c|) (x_c = the column before the last update),
-// the same order as Householder QR's normwise backward error; the parity suite checks R to 1e-10.
-template <int RQ>
+template <int RQ, bool kPreload>
 __device__ __forceinline__ void panel_factor_lazy(double* __restrict__ Bs, int lds, int brows, int j0,
                                                   double* __restrict__ R, int npad, const double* __restrict__ Rd,
                                                   double* __restrict__ Tm, double* __restrict__ red, int lane,
@@ -154,6 +138,15 @@ __device__ __forceinline__ void panel_factor_lazy(double* __restrict__ Bs, int l
   double trow[kNB], rmine[kNB], f[kNB];
 #pragma unroll
   for (int c = 0; c < kNB; ++c) trow[c] = rmine[c] = f[c] = 0.0;
+  // R(j, j) and R(j, j+1) are not touched by the panel's earlier reflectors (reflector i only changes
+  // R row i), so the diagonal and first off-diagonal are loaded up front, off the per-column chain
+  // (kPreload false: the register-capped two-CTAs-per-SM build reads them when needed instead)
+  double ralpha[kNB], rnext[kNB];
+#pragma unroll
+  for (int c = 0; c < kNB; ++c) {
+    ralpha[c] = kPreload ? Rd[c * kNB + c] : 0.0;
+    rnext[c] = (kPreload && c + 1 < kNB) ? Rd[c * kNB + c + 1] : 0.0;
+  }
   const int rc = lane & 7, rq = lane >> 3;
   double scale_prev = 0.0;
   // dots of step 0
@@ -188,7 +181,7 @@ __device__ __forceinline__ void panel_factor_lazy(double* __restrict__ Bs, int l
       d[js - 1] *= scale_prev;
     }
     // (C) reflector scalars
-    const double alpha = Rd[js * kNB + js];
+    const double alpha = kPreload ? ralpha[js] : Rd[js * kNB + js];
     double tau = 0.0, scale = 0.0, beta = alpha;
     if (d[js] > 0.0) {
       const double ss = fma(alpha, alpha, d[js]);
@@ -200,7 +193,7 @@ __device__ __forceinline__ void panel_factor_lazy(double* __restrict__ Bs, int l
     }
     // (D) critical: next pivot's factor, eager update of the next pivot column, next step's dots
     if (js + 1 < kNB) {
-      const double rjn = Rd[js * kNB + js + 1];
+      const double rjn = kPreload ? rnext[js] : Rd[js * kNB + js + 1];
       const double twn = tau * fma(scale, d[js + 1], rjn);
       f[js + 1] = twn * scale;
       if (lane == js + 1) rmine[js] = rjn - twn;
@@ -536,7 +529,7 @@ __device__ __forceinline__ void lookahead_pair(double* __restrict__ Bs, int lds,
 //   GEMM warps : wait PanelDone(p) -> arrive ColsReady(p+1) -> update column blocks p+2.. with panel p
 // so panel p+1 is factored while the trailing update of panel p runs.  V_p lives in the block's
 // panel-p columns (never touched again this block); T and the staged R rows are double-buffered.
-template <int RQ>
+template <int RQ, bool kPreload>
 __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src, int64_t nrows, int64_t ldsrc,
                           int ncols, const TqGeom g, bool triangular, bool init_zero,
                           double* __restrict__ stats_out, double* smem) {
@@ -594,7 +587,7 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
         if (p > p0) named_sync(kBarColsReady, kTqThreads);
         TQ_RESOLVE(Rdg);
         TQ_TRACE(1);
-        panel_factor_lazy<RQ>(Bs, lds, brows, j0, R, npad, Rdc, Tm + buf * kNB * kNB, red, lane, tq_p);
+        panel_factor_lazy<RQ, kPreload>(Bs, lds, brows, j0, R, npad, Rdc, Tm + buf * kNB * kNB, red, lane, tq_p);
         TQ_TRACE(2);
         named_arrive(kBarPanelDone, kTqThreads);
         if (kPairLookahead && more) {
@@ -666,7 +659,7 @@ __global__ void __launch_bounds__(kTqThreads, MINB)
   const int64_t cnt = max64(0, min64(rows_per_cta, m - r0));
   double* R = slots + (int64_t)blockIdx.x * g.npad * g.npad;
   double* st = stats ? stats + (int64_t)blockIdx.x * 2 * g.npad : nullptr;
-  tsqr_fold<RQ>(R, x + r0 * ldx, cnt, ldx, g.n, g, false, true, st, smem);
+  tsqr_fold<RQ, MINB == 1>(R, x + r0 * ldx, cnt, ldx, g.n, g, false, true, st, smem);
 }
 
 // One level of the binary-counter tree: slot[q*2^L] = qr([slot[q*2^L]; slot[q*2^L + 2^(L-1)]]),
@@ -685,7 +678,7 @@ __global__ void __launch_bounds__(kTqThreads, MINB)
     dst = fold_dst;
     srcs = fold_src;
   }
-  tsqr_fold<RQ>(slots + dst * ss, slots + srcs * ss, g.npad, g.npad, g.npad, g, true, false, nullptr, smem);
+  tsqr_fold<RQ, MINB == 1>(slots + dst * ss, slots + srcs * ss, g.npad, g.npad, g.npad, g, true, false, nullptr, smem);
 }
 
 // ---------------------------------------------------------------------------
