@@ -36,6 +36,7 @@ for w in (1, 2, 3, 4, 5, 6, 7):
 lw = 4 if np.nansum(t[4, :, 3]) > 0 else 1
 la_start = [t[lw, p, 3] - t[0, p, 2] for p in range(P - 1)]
 la_to_panel = [t[0, p + 1, 1] - t[lw, p, 4] for p in range(P - 1)]
+print("  per panel: panel done -> lookahead start", [int(v) for v in la_start])
 print(f"panel done -> lookahead start {np.nanmean(la_start):.0f}, lookahead end -> next panel start {np.nanmean(la_to_panel):.0f}, panel start -> col0 {np.nanmean([d(0,p,1,10) for p in range(P)]):.0f}, col7 end -> panel done {np.nanmean([d(0,p,37,2) for p in range(P)]):.0f}")
 tot = t[0, P - 1, 2] - t[0, 0, 1]
 print(f"block span (panel 0 start -> last panel done): {tot:.0f} clk = {tot / P:.0f} per panel")
