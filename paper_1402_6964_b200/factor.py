@@ -334,15 +334,46 @@ def _is_device(data) -> bool:
 HOST_BATCH_BYTES = 1 << 30  # rows per PCIe batch: ~1 GiB of X
 
 
-def _iter_nodes(chunks, engine: _PassEngine):
-    """Yield (node, n_input_chunks) for the stream.  Device chunks reduce in
-    place; host chunks are batched and double-buffered over a copy stream."""
+def _device_batch(items):
+    """One device matrix for consecutive device chunks with contiguous row offsets: a single strided view
+    when the chunks are adjacent slices of one allocation (the usual `x[o:o + c]` pattern), else a copy."""
     t = dv.torch()
+    if len(items) == 1:
+        return items[0][1]
+    first = items[0][1]
+    ld = first.stride(0) if first.shape[0] > 1 else first.shape[1]
+    adjacent = True
+    ptr = first.data_ptr()
+    for _, x in items:
+        if x.data_ptr() != ptr or x.stride(1) != 1 or (x.shape[0] > 1 and x.stride(0) != ld):
+            adjacent = False
+            break
+        ptr += x.shape[0] * ld * x.element_size()
+    rows = sum(int(x.shape[0]) for _, x in items)
+    if adjacent:
+        try:
+            return t.as_strided(first, (rows, first.shape[1]), (ld, 1))
+        except RuntimeError:  # outside the first tensor's storage: fall back to a copy
+            pass
+    return t.cat([x for _, x in items], dim=0)
+
+
+def _iter_nodes(chunks, engine: _PassEngine):
+    """Yield (node, n_input_chunks) for the stream.  Consecutive device chunks with contiguous row offsets
+    are reduced as one batch (up to ~1 GiB; a small chunk alone would occupy a fraction of the GPU —
+    8192-row chunks run at 9 GB/s one by one); host chunks are batched and double-buffered over a copy
+    stream.  Batching changes only the (deterministic) combination order, i.e. rounding, never the
+    reported chunk count or tree depth."""
     dev = dv.require_device()
     pending_host = []
+    pending_dev = []  # (row_offset, device matrix)
+    dev_rows = 0
 
     def flush_host(items):
         yield from _reduce_host(items, engine, dev)
+
+    def flush_dev():
+        yield engine.reduce(_device_batch(pending_dev), pending_dev[0][0]), len(pending_dev)
 
     for ch in chunks:
         if _is_device(ch.data):
@@ -352,15 +383,32 @@ def _iter_nodes(chunks, engine: _PassEngine):
             x = dv.as_device_matrix(ch.data)
             if x.shape[0] < 1:
                 raise UsageError(f"chunk must have at least one row, got shape {tuple(x.shape)}")
-            yield engine.reduce(x, int(ch.row_offset)), 1
+            off = int(ch.row_offset)
+            if pending_dev:
+                last_off, last = pending_dev[-1]
+                # adjacent slices of one allocation batch without limit (a view); others are copied, <= ~1 GiB
+                ld = last.stride(0) if last.shape[0] > 1 else last.shape[1]
+                adjacent = (x.data_ptr() == last.data_ptr() + last.shape[0] * ld * last.element_size()
+                            and (x.shape[0] == 1 or x.stride(0) == ld))
+                cap = max(1, HOST_BATCH_BYTES // (8 * int(last.shape[1])))
+                if (x.shape[1] != last.shape[1] or off != last_off + int(last.shape[0])
+                        or (not adjacent and dev_rows + x.shape[0] > cap)):
+                    yield from flush_dev()
+                    pending_dev, dev_rows = [], 0
+            pending_dev.append((off, x))
+            dev_rows += int(x.shape[0])
         else:
+            if pending_dev:
+                yield from flush_dev()
+                pending_dev, dev_rows = [], 0
             pending_host.append(ch)
             if len(pending_host) >= 4096:
                 yield from flush_host(pending_host)
                 pending_host = []
+    if pending_dev:
+        yield from flush_dev()
     if pending_host:
         yield from flush_host(pending_host)
-    del t
 
 
 def _reduce_host(chunks, engine: _PassEngine, dev):

@@ -98,6 +98,39 @@ def test_stream_pass_matches_reference(golden_tsqr, name, size, where):
     assert rel_err(rtr, x.T @ x) <= 1e-12
 
 
+def test_device_chunk_batching(oracle):
+    """Consecutive device chunks are reduced as one batch: adjacent slices through a strided view,
+    separately allocated chunks through a copy, a row-offset gap splits the batch.  Results, chunk count
+    and tree depth must not depend on how the stream is cut."""
+    rng = np.random.default_rng(21)
+    m, n = 50_000, 48
+    x = rng.uniform(0, 1, (m, n))
+    xd = dev(x)
+    whole = tb.stream_pass([tb.RowChunk(0, xd)], sketch_rows=16, seed=4)
+    want = oracle.factor_chunk(x)
+    assert rel_err(whole.factor.entries, want) <= R_TOL
+    for rows in (8192, 777, 1):
+        cuts = list(range(0, m, rows)) if rows > 1 else list(range(0, 40)) + [40]
+        if rows == 1:  # first 40 rows one by one, then the rest
+            pieces = [(o, xd[o:o + 1]) for o in range(40)] + [(40, xd[40:])]
+        else:
+            pieces = [(o, xd[o:o + rows]) for o in cuts]
+        res = tb.stream_pass([tb.RowChunk(o, p) for o, p in pieces], sketch_rows=16, seed=4)
+        assert rel_err(res.factor.entries, want) <= R_TOL
+        assert rel_err(res.sketch.entries, whole.sketch.entries) <= 1e-12
+        assert res.chunks == len(pieces) and res.tree_depth == len(pieces).bit_length() and res.rows == m
+    # separately allocated chunks (copy path)
+    sep = [tb.RowChunk(o, dev(x[o:o + 5000])) for o in range(0, m, 5000)]
+    res = tb.stream_pass(sep, sketch_rows=16, seed=4)
+    assert rel_err(res.factor.entries, want) <= R_TOL
+    assert rel_err(res.sketch.entries, whole.sketch.entries) <= 1e-12
+    # reordered chunks (non-contiguous offsets): every chunk is its own batch, same factor
+    rev = [tb.RowChunk(o, xd[o:o + 10_000]) for o in range(m - 10_000, -1, -10_000)]
+    res = tb.stream_pass(rev, sketch_rows=16, seed=4)
+    assert rel_err(res.factor.entries, want) <= R_TOL
+    assert rel_err(res.sketch.entries, whole.sketch.entries) <= 1e-12
+
+
 @pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 9, 15, 16, 17, 25, 31, 33, 64, 100, 127, 200, 255, 256, 300, 512])
 def test_factor_matches_oracle_many_widths(oracle, n):
     rng = np.random.default_rng(n)
