@@ -62,3 +62,25 @@ def test_fullsize_sketch_linearity(x_big):
     assert rel_err(s_a + s_b, s_all) <= 1e-12
     s2 = dv.sketch(x_big[:h] * 2.0, 0, 9, 128).cpu().numpy()
     assert np.array_equal(s2, 2.0 * s_a)
+
+
+def test_fullsize_narrow_c4_shape():
+    """C4 width (n = 25, warp-chain leaf + warp-pair tree) at 2^26 rows: R^T R = X^T X against the
+    device Gram, stats agreement, split invariance."""
+    m = 1 << 26
+    spec = synthetic.config("C4", m=m)
+    x = synthetic.generate(spec)
+    r, l1, sq = dv.tsqr(x)
+    g, gl1, _ = dv.gram(x)
+    rn, gn = r.cpu().numpy(), g.cpu().numpy()
+    assert np.array_equal(np.tril(rn, -1), np.zeros_like(rn)) and (np.diagonal(rn) >= 0).all()
+    assert rel_err(rn.T @ rn, gn) <= 1e-10
+    np.testing.assert_allclose(l1.cpu().numpy(), gl1.cpu().numpy(), rtol=1e-12)
+    np.testing.assert_allclose(sq.cpu().numpy(), np.diagonal(gn), rtol=1e-12)
+    h = m // 3 + 7
+    r1, _, _ = dv.tsqr(x[:h])
+    r2, _, _ = dv.tsqr(x[h:])
+    both = tb.combine(tb.TriangularFactor(r1.cpu().numpy()), tb.TriangularFactor(r2.cpu().numpy()))
+    assert rel_err(both.entries, rn) <= 1e-12
+    del x
+    torch.cuda.empty_cache()
