@@ -17,8 +17,9 @@ namespace tsnmf {
 #ifndef TSNMF_GRAM_WARPS
 #define TSNMF_GRAM_WARPS 8
 #endif
-constexpr int kGrWarps = TSNMF_GRAM_WARPS;   // 2 per SMSP; 12 / 16 measured slower (fewer tiles per warp, spills)
-constexpr int kGrThreads = 32 * kGrWarps;
+constexpr int kGrWarps = TSNMF_GRAM_WARPS;   // narrow widths: 2 warps per SMSP
+constexpr int kGrWarpsWide = 16;             // n > 192: 4 warps per SMSP hide the fragment-load latency
+                                             // better (+2..6% at n = 200..512; slower for narrow widths)
 constexpr int kGrSpwMax = 96 / kGrWarps;     // super-tiles per warp (96 per CTA = one group at n <= 208)
 constexpr int kGrBrMax = 256;  // rows per stage (halved until the double buffer fits)
 
@@ -29,6 +30,7 @@ struct GrGeom {
   int nst;      // super-tiles in the upper triangle
   int ks;       // k-slices per CTA (warps sharing a super-tile set, splitting the rows)
   int spw;      // super-tiles per warp (kernel template: 1, 3, 6, 10 or 12)
+  int warps;    // warps per CTA (kernel template: 8 or 16)
   int spc;      // super-tiles per CTA (tile group) = (8 / ks) * spw
   int groups;   // tile groups
   int br;       // rows per stage
@@ -49,8 +51,8 @@ __host__ __device__ inline void st_coords(int idx, int ns, int* P, int* Q) {
 // Warp w = kslice + ks * wi: k-slice `kslice` takes the 4-row k-steps i/4 = kslice (mod ks); warp index
 // wi within the slice owns a contiguous run of SPW super-tiles (consecutive super-tiles mostly share
 // their row P, so the A fragments are reused).  Partials: [split][kslice][supertile][16][16].
-template <int SPW>
-__global__ void __launch_bounds__(kGrThreads, 1)
+template <int SPW, int WARPS>
+__global__ void __launch_bounds__(32 * WARPS, 1)
     gram_kernel(const double* __restrict__ x, int64_t m, int64_t ldx, GrGeom g, double* __restrict__ partial,
                 double* __restrict__ l1part) {
   extern __shared__ __align__(16) double smem[];
@@ -78,10 +80,13 @@ __global__ void __launch_bounds__(kGrThreads, 1)
   for (int u = 0; u < SPW; ++u)
 #pragma unroll
     for (int t = 0; t < 4; ++t) acc[u][t][0] = acc[u][t][1] = 0.0;
-  double l1a[2] = {0.0, 0.0};
+  constexpr int kL1H = (512 + (32 * WARPS) - 1) / (32 * WARPS);  // columns per thread for n <= 512
+  double l1a[kL1H];
+#pragma unroll
+  for (int h = 0; h < kL1H; ++h) l1a[h] = 0.0;
   const bool do_l1 = (group == 0) && (l1part != nullptr);
   // column l1: narrow matrices split each column's rows over l1_ph thread phases
-  const int l1_ph = g.npad <= kGrThreads / 2 ? kGrThreads / g.npad : 1;
+  const int l1_ph = g.npad <= (32 * WARPS) / 2 ? (32 * WARPS) / g.npad : 1;
   const int l1_c = tid % g.npad, l1_r0 = tid / g.npad;
   const int frag_col = (lane >> 2) ^ ((lane & 2) << 1);  // swizzled slab fragment: row i + l%4, col l/4
 
@@ -112,8 +117,8 @@ __global__ void __launch_bounds__(kGrThreads, 1)
         }
       } else {
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int col = tid + h * kGrThreads;
+        for (int h = 0; h < kL1H; ++h) {
+          const int col = tid + h * (32 * WARPS);
           if (col < g.n) {
             // 4 independent chains so the adds pipeline (br % 4 == 0; rows 4j+2, 4j+3 are XOR-4 swizzled);
             // the summation order is fixed, so the result stays deterministic
@@ -174,8 +179,8 @@ __global__ void __launch_bounds__(kGrThreads, 1)
       }
     } else {
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int col = tid + h * kGrThreads;
+      for (int h = 0; h < kL1H; ++h) {
+        const int col = tid + h * (32 * WARPS);
         if (col < g.npad) l1part[split * g.npad + col] = l1a[h];
       }
     }
@@ -223,17 +228,23 @@ GrGeom gr_geom(int64_t m, int n, int sms) {
   {
     const int spws[5] = {1, 3, 6, 10, 12};
     int best_slots = 1 << 30;
+    g.warps = kGrWarps;
     g.spw = kGrSpwMax;
     g.ks = 1;
     for (int wps = 1; wps <= kGrWarps; wps *= 2)
       for (int i = 0; i < 5; ++i)
-        if (wps * spws[i] >= g.nst && wps * spws[i] < best_slots) {
+        if (spws[i] <= kGrSpwMax && wps * spws[i] >= g.nst && wps * spws[i] < best_slots) {
           best_slots = wps * spws[i];
           g.spw = spws[i];
           g.ks = kGrWarps / wps;
         }
+    if (g.nst > 80) {  // wide (n > 192): 16 warps x 6 super-tiles (same 96 per tile group, half the registers)
+      g.warps = kGrWarpsWide;
+      g.spw = 96 / kGrWarpsWide;
+      g.ks = 1;
+    }
   }
-  g.spc = (kGrWarps / g.ks) * g.spw;
+  g.spc = (g.warps / g.ks) * g.spw;
   g.groups = (int)ceil_div(g.nst, g.spc);
   g.br = kGrBrMax;
   while (g.br > 8 && 2 * g.br * g.lds * 8 > 227 * 1024) g.br /= 2;
@@ -265,15 +276,16 @@ size_t gram_workspace_bytes(int64_t m, int n) {
   return sizeof(double) * (size_t)(splits * g.ks * g.nst * 256 + splits * g.npad) + 256;
 }
 
-template <int SPW>
+template <int SPW, int WARPS>
 int gram_launch(const double* x, int64_t m, int64_t ldx, const GrGeom& g, double* partial, double* l1part,
                 int64_t splits, size_t smem, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    TSNMF_CUDA_CHECK(cudaFuncSetAttribute(gram_kernel<SPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+    TSNMF_CUDA_CHECK((cudaFuncSetAttribute(gram_kernel<SPW, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           232448)));
     attr = true;
   }
-  gram_kernel<SPW><<<dim3(g.groups, (unsigned)splits), kGrThreads, smem, st>>>(x, m, ldx, g, partial, l1part);
+  gram_kernel<SPW, WARPS><<<dim3(g.groups, (unsigned)splits), 32 * WARPS, smem, st>>>(x, m, ldx, g, partial, l1part);
   TSNMF_LAUNCH_CHECK();
   return kOk;
 }
@@ -290,12 +302,16 @@ int gram_run(const double* x, int64_t m, int n, int64_t ldx, double* gout, int64
   const size_t smem = gr_smem(g);
   prof_mark(kProfGram, true, st);
   int rc = kOk;
-  switch (g.spw) {
-    case 1: rc = gram_launch<1>(x, m, ldx, g, partial, l1 ? l1part : nullptr, splits, smem, st); break;
-    case 3: rc = gram_launch<3>(x, m, ldx, g, partial, l1 ? l1part : nullptr, splits, smem, st); break;
-    case 6: rc = gram_launch<6>(x, m, ldx, g, partial, l1 ? l1part : nullptr, splits, smem, st); break;
-    case 10: rc = gram_launch<10>(x, m, ldx, g, partial, l1 ? l1part : nullptr, splits, smem, st); break;
-    default: rc = gram_launch<12>(x, m, ldx, g, partial, l1 ? l1part : nullptr, splits, smem, st); break;
+  if (g.warps == kGrWarpsWide) {
+    rc = gram_launch<96 / kGrWarpsWide, kGrWarpsWide>(x, m, ldx, g, partial, l1 ? l1part : nullptr, splits, smem, st);
+  } else {
+    switch (g.spw) {
+      case 1: rc = gram_launch<1, kGrWarps>(x, m, ldx, g, partial, l1 ? l1part : nullptr, splits, smem, st); break;
+      case 3: rc = gram_launch<3, kGrWarps>(x, m, ldx, g, partial, l1 ? l1part : nullptr, splits, smem, st); break;
+      case 6: rc = gram_launch<6, kGrWarps>(x, m, ldx, g, partial, l1 ? l1part : nullptr, splits, smem, st); break;
+      case 10: rc = gram_launch<10, kGrWarps>(x, m, ldx, g, partial, l1 ? l1part : nullptr, splits, smem, st); break;
+      default: rc = gram_launch<12, kGrWarps>(x, m, ldx, g, partial, l1 ? l1part : nullptr, splits, smem, st); break;
+    }
   }
   if (rc) return rc;
   prof_mark(kProfGram, false, st);
