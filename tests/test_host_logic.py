@@ -160,6 +160,37 @@ def test_sweep_host(golden_select):
         tb.sweep(rr, stats, ["gp"], [1])
 
 
+def test_sweep_report_files(golden_select, tmp_path):
+    import csv
+    import json
+
+    rr = golden_select["m2"]
+    stats = tb.ColumnStats(l1=golden_select["m2_l1"].copy(), l2=np.ones(rr.shape[1]))
+    rep = tb.sweep(rr, stats, ["spa"], range(1, 4))
+    rep.write_json(tmp_path / "s.json")
+    rep.write_csv(tmp_path / "s.csv")
+    assert json.loads((tmp_path / "s.json").read_text()) == rep.to_json_dict()
+    rows = list(csv.reader(open(tmp_path / "s.csv")))
+    assert rows[0] == ["r", "algorithm", "residual", "seconds"] and len(rows) == 4
+    assert [float(r[2]) for r in rows[1:]] == [rep.residuals("spa")[r] for r in (1, 2, 3)]
+
+
+def test_gram_result_cholesky():
+    from paper_1402_6964_b200.factor import GramResult
+
+    x = np.random.default_rng(3).standard_normal((500, 12))
+    g = GramResult(gram=x.T @ x, stats=tb.ColumnStats(l1=np.abs(x).sum(0), l2=np.sqrt((x * x).sum(0))),
+                   rows=500, chunks=1, tree_depth=1)
+    r = g.cholesky_factor().entries
+    q = np.linalg.qr(x, mode="r")
+    q = q * np.sign(np.diagonal(q))[:, None]
+    assert np.abs(r - q).max() <= 1e-10 * np.abs(q).max()
+    bad = GramResult(gram=-np.eye(3), stats=tb.ColumnStats(l1=np.ones(3), l2=np.ones(3)), rows=3, chunks=1,
+                     tree_depth=1)
+    with pytest.raises(tb.NumericalError):
+        bad.cholesky_factor()
+
+
 def test_nnls_input_checks():
     with pytest.raises(tb.UsageError):
         nonneg.nnls_solve(np.ones((3, 2)), np.ones(4))
