@@ -17,6 +17,8 @@
 // next panel.  Narrow matrices (n <= 32) use a warp-per-chain leaf instead (tsqr_small_leaf_kernel).  Leaves are then combined in the reference TreeReducer order (perfect
 // binary levels over the leaf index, then a fold of the leftover subtrees), each combine being the same
 // structured QR with the second factor's rows as data (triangular: panels left of the block are skipped).
+#include <utility>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -839,6 +841,235 @@ __global__ void __launch_bounds__(32 * kSmWarps)
   small_store_r<NC>(R, npad, n, rcol, lane);
 }
 
+// ---------------------------------------------------------------------------
+// Narrow leaf, register-block version (n <= 32; the default narrow leaf): one chain per warp (CTA = one
+// warp), blocks of 32*S rows held in registers (lane l: rows l, l+32, ..), R in shared memory.
+// The per-column fixed costs of the chain (butterfly norm, reflector scalars, the column sums of the
+// products through shared memory, the broadcast of tau*w) are paid once per 32*S rows instead of once per
+// 32, so the instruction count per row drops ~S-fold for those parts.  Blocks are staged by the bulk-copy
+// (TMA) engine into a dense buffer (one instruction per block, completion on an mbarrier) when X is
+// contiguous with odd n (conflict-free row reads at stride n), else by cp.async at an odd stride; the
+// next block's copy is issued as soon as the current one is in registers, so it overlaps the fold.
+// Same reflector algebra as small_fold_block ([e_j; v], dlarfg conventions, tsqr.py:129-153 semantics).
+struct WlGeom {
+  int n, npad;
+  int ls;        // stage row stride (odd): n for odd n, n + 1 otherwise
+  int pld;       // product tile row stride (== 2 mod 4: conflict-free 16-byte row writes)
+  int stage_off, prod_off, r_off, tw_off;  // doubles from the CTA's smem base (even: 16-byte aligned)
+  int total;     // doubles
+};
+
+// 1/sqrt(a), 1/a (a > 0, any finite magnitude incl. subnormal) without branches: the argument is scaled
+// by an even power of two into the range where the .ftz approximation + two Newton steps is accurate
+// (~1 ulp), and the result scaled back exactly.  Branch-free so the column step stays one basic block.
+__device__ __forceinline__ double rsqrt_nb(double a) {
+  const double sc = a < 0x1p-900 ? 0x1p+600 : (a > 0x1p+900 ? 0x1p-600 : 1.0);
+  const double as = a * sc * sc;
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(as));
+  const double h = 0.5 * as;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return y * sc;
+}
+__device__ __forceinline__ double rcp_nb(double a) {
+  const double sc = a < 0x1p-900 ? 0x1p+600 : (a > 0x1p+900 ? 0x1p-600 : 1.0);
+  const double as = a * sc;
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(as));
+  y = y * fma(-as, y, 2.0);
+  y = y * fma(-as, y, 2.0);
+  return y * sc;
+}
+
+template <int N, int S>
+__global__ void __launch_bounds__(32)
+    tsqr_warp_leaf_kernel(const double* __restrict__ x, int64_t m, int64_t ldx, int64_t rows_per_warp, WlGeom g,
+                          double* __restrict__ slots, double* __restrict__ stats) {
+  extern __shared__ __align__(16) double smem[];
+  constexpr int BR = 32 * S;
+  const int lane = threadIdx.x;
+  const int ls = g.ls, pld = g.pld;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+  double* stg = smem + g.stage_off;
+  double* P = smem + g.prod_off;
+  double* Rs = smem + g.r_off;  // R(i, c) at Rs[i * N + c]
+  double* TW = smem + g.tw_off;
+  const int64_t leaf = blockIdx.x;
+  const int64_t rbeg = leaf * rows_per_warp;
+  const int64_t rend = min64(m, rbeg + rows_per_warp);
+  for (int i = lane; i < N * N; i += 32) Rs[i] = 0.0;
+  for (int i = lane; i < N + 1; i += 32) TW[i] = 0.0;
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncwarp();
+  const bool dense = (ldx == N) && (N & 1) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  // stage rows [r0, r0 + cnt); returns true when the bulk engine was used (completion on `bar`)
+  auto issue = [&](int64_t r0, int cnt) -> bool {
+    const double* src = x + r0 * ldx;
+    if (dense && (cnt & 1) == 0) {  // r0 is even (rows_per_warp % BR == 0), so src is 16-byte aligned
+      if (lane == 0) {
+        fence_proxy_async_smem();  // the warp's reads of the previous block (ordered by __syncwarp) come first
+        mbar_arrive_expect_tx(bar, (unsigned)(cnt * N * 8));
+        bulk_copy_g2s(stg, src, (unsigned)(cnt * N * 8), bar);
+      }
+      return true;
+    }
+    for (GridWalk it(lane, 32, N); it.r < cnt; it.next()) cp_async8(stg + it.r * ls + it.c, src + it.r * ldx + it.c);
+    cp_async_commit();
+    return false;
+  };
+  double l1 = 0.0, sq = 0.0;  // lane c: column c
+  unsigned phase = 0;
+  bool bulk = rbeg < rend ? issue(rbeg, (int)min64(BR, rend - rbeg)) : false;
+  for (int64_t r0 = rbeg; r0 < rend; r0 += BR) {
+    const int cnt = (int)min64(BR, rend - r0);
+    if (bulk) {
+      mbar_wait_parity(bar, phase);
+      phase ^= 1u;
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncwarp();
+    double xr[S][N];
+#pragma unroll
+    for (int q = 0; q < S; ++q) {
+      const int row = lane + 32 * q;
+#pragma unroll
+      for (int c = 0; c < N; ++c) xr[q][c] = row < cnt ? stg[row * ls + c] : 0.0;
+    }
+    if (stats && lane < N) {
+      double a0 = 0.0, a1 = 0.0, q0 = 0.0, q1 = 0.0;
+      int row = 0;
+      for (; row + 2 <= cnt; row += 2) {
+        const double v0 = stg[row * ls + lane], v1 = stg[(row + 1) * ls + lane];
+        a0 += fabs(v0);
+        a1 += fabs(v1);
+        q0 = fma(v0, v0, q0);
+        q1 = fma(v1, v1, q1);
+      }
+      if (row < cnt) {
+        const double v0 = stg[row * ls + lane];
+        a0 += fabs(v0);
+        q0 = fma(v0, v0, q0);
+      }
+      l1 += a0 + a1;
+      sq += q0 + q1;
+    }
+    __syncwarp();  // the whole warp is done reading the stage buffer
+    if (r0 + BR < rend) bulk = issue(r0 + BR, (int)min64(BR, rend - r0 - BR));
+    // Column steps, straight-line code (N, j, c compile-time; no branches): lane c (j < c < N) owns
+    // w_c = R(j, c) + sum over the block of v x[:, c].  Column j+1 is updated first; the remaining
+    // columns' updates of step j are deferred into step j+1, behind its norm butterfly.
+    double v_prev[S];
+#pragma unroll
+    for (int q = 0; q < S; ++q) v_prev[q] = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      // R row j is only changed by reflector j, so R(j, c) is read up front (off the chain)
+      const double rjc = Rs[j * N + (lane < N ? lane : 0)];
+      double d = 0.0;
+#pragma unroll
+      for (int q = 0; q < S; ++q) d = fma(xr[q][j], xr[q][j], d);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+      // deferred updates of step j-1 (columns j+1 .. N-1; TW still holds step j-1's tau w), overlapping the
+      // butterfly
+      if (j > 0) {
+        int c = j + 1;
+        if (c & 1) {
+          const double t = TW[c];
+#pragma unroll
+          for (int q = 0; q < S; ++q) xr[q][c] = fma(-t, v_prev[q], xr[q][c]);
+          ++c;
+        }
+#pragma unroll
+        for (; c < N; c += 2) {
+          const double2 t = *reinterpret_cast<const double2*>(TW + c);  // TW has N + 1 (even-rounded) slots
+#pragma unroll
+          for (int q = 0; q < S; ++q) {
+            xr[q][c] = fma(-t.x, v_prev[q], xr[q][c]);
+            if (c + 1 < N) xr[q][c + 1] = fma(-t.y, v_prev[q], xr[q][c + 1]);
+          }
+        }
+      }
+      const double alpha = __shfl_sync(0xffffffffu, rjc, j);
+      const bool live = d > 0.0;
+      const double ss = live ? fma(alpha, alpha, d) : 1.0;
+      const double inv = rsqrt_nb(ss);
+      const double nrm = ss * inv;
+      const double beta = live ? -copysign(nrm, alpha) : alpha;
+      const double tau = live ? fma(fabs(alpha), inv, 1.0) : 0.0;
+      const double scale = live ? copysign(rcp_nb(fabs(alpha) + nrm), alpha) : 0.0;
+      double v[S];
+#pragma unroll
+      for (int q = 0; q < S; ++q) v[q] = xr[q][j] * scale;
+      if (j + 1 < N) {
+        // products p_c = sum_q v_q x_q[c] (this lane's rows) -> row `lane` of the product tile
+        double* prow = P + lane * pld;
+        int c = j + 1;
+        if (c & 1) {
+          double p = 0.0;
+#pragma unroll
+          for (int q = 0; q < S; ++q) p = fma(v[q], xr[q][c], p);
+          prow[c] = p;
+          ++c;
+        }
+#pragma unroll
+        for (; c < N; c += 2) {
+          double p0 = 0.0, p1 = 0.0;
+#pragma unroll
+          for (int q = 0; q < S; ++q) {
+            p0 = fma(v[q], xr[q][c], p0);
+            if (c + 1 < N) p1 = fma(v[q], xr[q][c + 1], p1);
+          }
+          if (c + 1 < N)
+            *reinterpret_cast<double2*>(prow + c) = make_double2(p0, p1);
+          else
+            prow[c] = p0;
+        }
+        __syncwarp();
+        // every lane sums its column of the tile (lanes outside (j, N) read bytes they then discard)
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+        for (int row = 0; row < 32; row += 4) {
+          s0 += P[(row + 0) * pld + lane];
+          s1 += P[(row + 1) * pld + lane];
+          s2 += P[(row + 2) * pld + lane];
+          s3 += P[(row + 3) * pld + lane];
+        }
+        const double tw = tau * (rjc + ((s0 + s1) + (s2 + s3)));
+        if (lane > j && lane < N) {
+          Rs[j * N + lane] = rjc - tw;
+          TW[lane] = tw;
+        }
+      }
+      if (lane == j) Rs[j * N + j] = beta;
+      if (j + 1 < N) {
+        __syncwarp();
+        // critical: the next pivot column now; the rest is deferred into step j+1
+        const double t = TW[j + 1];
+#pragma unroll
+        for (int q = 0; q < S; ++q) xr[q][j + 1] = fma(-t, v[q], xr[q][j + 1]);
+#pragma unroll
+        for (int q = 0; q < S; ++q) v_prev[q] = v[q];
+      }
+    }
+  }
+  __syncwarp();
+  double* R = slots + leaf * g.npad * g.npad;
+  if (lane < g.npad) {
+    for (int i = 0; i < g.npad; ++i)
+      R[(int64_t)i * g.npad + lane] = (i < N && lane < N && i <= lane) ? Rs[i * N + lane] : 0.0;
+    if (stats) {
+      stats[leaf * 2 * g.npad + lane] = lane < N ? l1 : 0.0;
+      stats[leaf * 2 * g.npad + g.npad + lane] = lane < N ? sq : 0.0;
+    }
+  }
+}
+
 // R_out (n x n, row-major, stride ldr) = sign-fixed upper triangle of slot 0 (tsqr.py:113-118).
 __global__ void tsqr_finalize_kernel(const double* __restrict__ slot, int npad, int n, double* __restrict__ r,
                                      int64_t ldr) {
@@ -993,13 +1224,55 @@ void tq_plan(const TqChoice& ch, int64_t m, int* nleaves, int64_t* rows_per_cta)
   *rows_per_cta = rpc;
 }
 
-// Narrow leaf plan (n <= 32): one chain per warp, 3 CTAs x 4 warps per SM, 32-row blocks.
+// Narrow leaves (n <= 32).  Default: the register-block warp leaf (tsqr_warp_leaf_kernel, 32*S-row blocks,
+// CTA = one warp); TSNMF_TSQR_WARPLEAF=0 selects the 32-row warp-chain leaf (tsqr_small_leaf_kernel) and
+// TSNMF_TSQR_SMALL=0 the shared-panel leaf.
 bool small_path(int n) {
   if (n > 32) return false;
   if (const char* e = getenv("TSNMF_TSQR_SMALL")) return atoi(e) != 0;
   return true;
 }
+bool warp_leaf_path(int n) {
+  if (!small_path(n)) return false;
+  if (const char* e = getenv("TSNMF_TSQR_WARPLEAF")) return atoi(e) != 0;
+  return true;
+}
+int small_nc(int n) { return n <= 8 ? 8 : (int)round_up(n, 4); }
+// rows per lane: as many as the 255-register budget holds without spilling (x block = S * n doubles)
+constexpr int warp_leaf_s_of(int n) { return n <= 20 ? 4 : (n <= 28 ? 3 : 2); }
+int warp_leaf_s(int n) { return warp_leaf_s_of(n); }
+WlGeom warp_leaf_geom(int n, int S) {
+  WlGeom g;
+  g.n = n;
+  g.npad = (int)round_up(n, kNB);
+  g.ls = (n & 1) ? n : n + 1;
+  g.pld = n + 1;
+  while (g.pld % 4 != 2) ++g.pld;
+  g.stage_off = 2;  // [0, 2): mbarrier
+  g.prod_off = g.stage_off + (int)round_up(32 * S * g.ls, 2);
+  g.r_off = g.prod_off + (int)round_up(32 * g.pld, 2);
+  g.tw_off = g.r_off + (int)round_up(n * n, 2);
+  g.total = g.tw_off + (int)round_up(n + 1, 2);
+  return g;
+}
+// resident warp leaves per SM: shared memory (228 KB per SM, 1 KB reserved per CTA) and registers
+// (<= 255 per thread -> 8 one-warp CTAs)
+int warp_leaf_per_sm(const WlGeom& g) {
+  const int bytes = (int)sizeof(double) * g.total + 1024;
+  int k = (228 * 1024) / bytes;
+  return k < 1 ? 1 : (k > 8 ? 8 : k);
+}
+void warp_leaf_plan(int n, int64_t m, int* nleaves, int64_t* rows_per_warp) {
+  const int S = warp_leaf_s(n);
+  const int64_t br = 32 * S;
+  const int64_t max_leaves = (int64_t)device_sms() * warp_leaf_per_sm(warp_leaf_geom(n, S));
+  int64_t leaves = max64(1, min64(max_leaves, ceil_div(m, br)));
+  const int64_t rpw = round_up(ceil_div(m, leaves), br);
+  *nleaves = (int)ceil_div(m, rpw);
+  *rows_per_warp = rpw;
+}
 
+// Warp-chain leaf plan: one chain per warp, 3 CTAs x 4 warps per SM, 32-row blocks.
 void small_plan(int64_t m, int* nleaves, int64_t* rows_per_warp) {
   const int64_t max_leaves = (int64_t)device_sms() * 3 * kSmWarps;
   int64_t leaves = max64(1, min64(max_leaves, ceil_div(m, 32)));
@@ -1009,21 +1282,17 @@ void small_plan(int64_t m, int* nleaves, int64_t* rows_per_warp) {
   *rows_per_warp = rpw;
 }
 
+void narrow_plan(int n, int64_t m, int* nleaves, int64_t* rows_per_warp) {
+  if (warp_leaf_path(n))
+    warp_leaf_plan(n, m, nleaves, rows_per_warp);
+  else
+    small_plan(m, nleaves, rows_per_warp);
+}
+
+// binary-counter tree over the narrow leaves (tsqr.py:213-230): perfect levels, then fold leftover subtrees
+// low -> high
 template <int NC>
-int small_launch(const double* x, int64_t m, int n, int64_t ldx, int64_t rpw, int nleaves, int npad, double* slots,
-                 double* stats, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    TSNMF_CUDA_CHECK(cudaFuncSetAttribute(tsqr_small_leaf_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)SmallLayout<NC>::bytes));
-    attr = true;
-  }
-  prof_mark(kProfTsqrLeaf, true, st);
-  tsqr_small_leaf_kernel<NC><<<nleaves / kSmWarps, 32 * kSmWarps, SmallLayout<NC>::bytes, st>>>(
-      x, m, n, ldx, rpw, npad, slots, stats);
-  TSNMF_LAUNCH_CHECK();
-  prof_mark(kProfTsqrLeaf, false, st);
-  // binary-counter tree (tsqr.py:213-230): perfect levels, then fold leftover subtrees low -> high
+int small_tree(int n, int nleaves, int npad, double* slots, cudaStream_t st) {
   prof_mark(kProfTsqrTree, true, st);
   for (int64_t span = 2; span <= nleaves; span *= 2) {
     const int64_t pairs = nleaves / span;
@@ -1045,6 +1314,52 @@ int small_launch(const double* x, int64_t m, int n, int64_t ldx, int64_t rpw, in
   }
   prof_mark(kProfTsqrTree, false, st);
   return kOk;
+}
+
+template <int N>
+int warp_leaf_launch(const double* x, int64_t m, int64_t ldx, int64_t rpw, int nleaves, double* slots, double* stats,
+                     cudaStream_t st) {
+  constexpr int S = warp_leaf_s_of(N);
+  const WlGeom g = warp_leaf_geom(N, S);
+  const int bytes = (int)sizeof(double) * g.total;
+  TSNMF_CUDA_CHECK(
+      cudaFuncSetAttribute(tsqr_warp_leaf_kernel<N, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  prof_mark(kProfTsqrLeaf, true, st);
+  tsqr_warp_leaf_kernel<N, S><<<nleaves, 32, bytes, st>>>(x, m, ldx, rpw, g, slots, stats);
+  TSNMF_LAUNCH_CHECK();
+  prof_mark(kProfTsqrLeaf, false, st);
+  return small_tree<(N <= 8 ? 8 : (N + 3) / 4 * 4)>(N, nleaves, g.npad, slots, st);
+}
+
+template <int... Ns>
+int warp_leaf_exact(int n, const double* x, int64_t m, int64_t ldx, int64_t rpw, int nleaves, double* slots,
+                    double* stats, cudaStream_t st, std::integer_sequence<int, Ns...>) {
+  int rc = kUsage;
+  ((n == Ns + 1 ? (rc = warp_leaf_launch<Ns + 1>(x, m, ldx, rpw, nleaves, slots, stats, st), 0) : 0), ...);
+  return rc;
+}
+
+// one instantiation per width (the column loop is straight-line code in n)
+int warp_leaf(const double* x, int64_t m, int n, int64_t ldx, int64_t rpw, int nleaves, double* slots, double* stats,
+              cudaStream_t st) {
+  return warp_leaf_exact(n, x, m, ldx, rpw, nleaves, slots, stats, st, std::make_integer_sequence<int, 32>{});
+}
+
+template <int NC>
+int small_launch(const double* x, int64_t m, int n, int64_t ldx, int64_t rpw, int nleaves, int npad, double* slots,
+                 double* stats, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    TSNMF_CUDA_CHECK(cudaFuncSetAttribute(tsqr_small_leaf_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)SmallLayout<NC>::bytes));
+    attr = true;
+  }
+  prof_mark(kProfTsqrLeaf, true, st);
+  tsqr_small_leaf_kernel<NC><<<nleaves / kSmWarps, 32 * kSmWarps, SmallLayout<NC>::bytes, st>>>(
+      x, m, n, ldx, rpw, npad, slots, stats);
+  TSNMF_LAUNCH_CHECK();
+  prof_mark(kProfTsqrLeaf, false, st);
+  return small_tree<NC>(n, nleaves, npad, slots, st);
 }
 
 int small_leaf(const double* x, int64_t m, int n, int64_t ldx, int64_t rpw, int nleaves, int npad, double* slots,
@@ -1083,7 +1398,7 @@ size_t tsqr_workspace_bytes(int64_t m, int n) {
   int nleaves;
   int64_t rpc;
   if (small_path(n))
-    small_plan(max64(m, 1), &nleaves, &rpc);
+    narrow_plan(n, max64(m, 1), &nleaves, &rpc);
   else
     tq_plan(ch, max64(m, 1), &nleaves, &rpc);
   const int64_t npad = ch.g.npad;
@@ -1105,7 +1420,7 @@ int tsqr_run(const double* x, int64_t m, int n, int64_t ldx, double* r, int64_t 
   int64_t rpc;
   const bool narrow = small_path(n);
   if (narrow)
-    small_plan(m, &nleaves, &rpc);
+    narrow_plan(n, m, &nleaves, &rpc);
   else
     tq_plan(ch, m, &nleaves, &rpc);
   const int64_t npad = ch.g.npad;
@@ -1115,7 +1430,9 @@ int tsqr_run(const double* x, int64_t m, int n, int64_t ldx, double* r, int64_t 
   double* stats = slots + (int64_t)nleaves * npad * npad;
   const bool want_stats = (l1 != nullptr) || (sumsq != nullptr);
   int rc;
-  if (narrow) {
+  if (narrow && warp_leaf_path(n)) {
+    rc = warp_leaf(x, m, n, ldx, rpc, nleaves, slots, want_stats ? stats : nullptr, st);
+  } else if (narrow) {
     rc = small_leaf(x, m, n, ldx, rpc, nleaves, (int)npad, slots, want_stats ? stats : nullptr, st);
   } else {
     rc = tq_dispatch(ch, x, m, ldx, slots, want_stats ? stats : nullptr, nleaves, rpc, st);
@@ -1151,6 +1468,14 @@ int tsqr_describe(int n, int64_t m, int* nb, int* brows, int* ctas_per_sm, int* 
   TqChoice ch;
   if (!tq_config(n, &ch)) return set_error(kUsage, "tsqr: n = %d too large", n);
   int64_t rpc;
+  if (warp_leaf_path(n)) {  // register-block warp leaf: "panel" 1 column, 32*S-row blocks, one warp per CTA
+    warp_leaf_plan(n, max64(m, 1), nleaves, &rpc);
+    const int S = warp_leaf_s(n);
+    *nb = 1;
+    *brows = 32 * S;
+    *ctas_per_sm = warp_leaf_per_sm(warp_leaf_geom(n, S));
+    return kOk;
+  }
   if (small_path(n)) {  // warp-per-chain leaf: "panel" 1 column, 32-row blocks, 3 CTAs (12 chains) per SM
     small_plan(max64(m, 1), nleaves, &rpc);
     *nb = 1;

@@ -157,7 +157,8 @@ def test_tall_shapes_and_tree_edges(oracle, m):
         assert rel_err(f.entries.T @ f.entries, x.T @ x) <= 1e-12
 
 
-@pytest.mark.parametrize("n,m", [(8, 33), (25, 1000), (25, 100_003), (32, 1_000_003), (17, 777_777), (25, 2_500_000)])
+@pytest.mark.parametrize("n,m", [(8, 33), (25, 1000), (25, 100_003), (32, 1_000_003), (17, 777_777), (25, 2_500_000),
+                                 (1, 5000), (2, 4099), (24, 300_001), (31, 65_537)])
 def test_narrow_warp_chain_path(oracle, monkeypatch, n, m):
     """n <= 32 runs one Householder chain per warp (many leaves, warp-level combine tree with leftover
     folds, partial 32-row blocks); it must agree with the oracle and with the shared-panel path."""
@@ -169,12 +170,35 @@ def test_narrow_warp_chain_path(oracle, monkeypatch, n, m):
     assert rel_err(r.cpu().numpy(), want) <= R_TOL
     np.testing.assert_allclose(l1.cpu().numpy(), np.abs(x).sum(0), rtol=1e-12)
     np.testing.assert_allclose(sq.cpu().numpy(), (x * x).sum(0), rtol=1e-12)
+    monkeypatch.setenv("TSNMF_TSQR_WARPLEAF", "0")  # the 32-row warp-chain leaf
+    r3, l13, _ = dv.tsqr(xd)
+    assert rel_err(r3.cpu().numpy(), want) <= R_TOL
+    np.testing.assert_allclose(l13.cpu().numpy(), np.abs(x).sum(0), rtol=1e-12)
+    monkeypatch.delenv("TSNMF_TSQR_WARPLEAF")
     monkeypatch.setenv("TSNMF_TSQR_SMALL", "0")
     r2, _, _ = dv.tsqr(xd)
     assert rel_err(r2.cpu().numpy(), r.cpu().numpy()) <= R_TOL
     assert dv.tsqr_plan(n, m)["panel"] == 8
     monkeypatch.delenv("TSNMF_TSQR_SMALL")
     assert dv.tsqr_plan(n, m)["panel"] == 1
+
+
+@pytest.mark.parametrize("n,m,ld", [(25, 100_001, 26), (25, 96 * 7 + 1, 25), (16, 50_000, 19), (25, 3, 25), (25, 25, 25)])
+def test_narrow_register_block_staging(oracle, n, m, ld):
+    """The register-block narrow leaf stages contiguous odd-width blocks with the bulk-copy engine and
+    everything else (row stride != n, odd tails) with cp.async; both must give the oracle's R."""
+    rng = np.random.default_rng(m + ld)
+    full = rng.uniform(0, 1, (m, ld))
+    x = full[:, :n]
+    xd = torch.as_tensor(full, device="cuda")[:, :n]
+    r, l1, sq = dv.tsqr(xd)
+    want = oracle.factor_chunk(np.ascontiguousarray(x))
+    if m >= n:
+        assert rel_err(r.cpu().numpy(), want) <= R_TOL
+    else:
+        assert rel_err(r.cpu().numpy().T @ r.cpu().numpy(), x.T @ x) <= 1e-12
+    np.testing.assert_allclose(l1.cpu().numpy(), np.abs(x).sum(0), rtol=1e-12)
+    np.testing.assert_allclose(sq.cpu().numpy(), (x * x).sum(0), rtol=1e-12)
 
 
 def test_combine_many_factors_tree_order(oracle):
