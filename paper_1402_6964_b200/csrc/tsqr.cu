@@ -862,6 +862,10 @@ struct WlGeom {
 // 1/sqrt(a), 1/a (a > 0, any finite magnitude incl. subnormal) without branches: the argument is scaled
 // by an even power of two into the range where the .ftz approximation + two Newton steps is accurate
 // (~1 ulp), and the result scaled back exactly.  Branch-free so the column step stays one basic block.
+__host__ __device__ constexpr int pow2ceil(int v) {  // v <= 32
+  return v <= 1 ? 1 : (v <= 2 ? 2 : (v <= 4 ? 4 : (v <= 8 ? 8 : (v <= 16 ? 16 : 32))));
+}
+
 __device__ __forceinline__ double rsqrt_nb(double a) {
   const double sc = a < 0x1p-900 ? 0x1p+600 : (a > 0x1p+900 ? 0x1p-600 : 1.0);
   const double as = a * sc * sc;
@@ -882,22 +886,34 @@ __device__ __forceinline__ double rcp_nb(double a) {
   return y * sc;
 }
 
+// CTA barrier every wl_sync(N) column steps (0: none).  The warps of a CTA run the same straight-line
+// column code; for wide blocks (N >= 24: ~150 KB of code per block fold) keeping them within a few columns
+// of each other lets them share instruction-cache lines (measured n=25: 871 -> 906 GB/s with 4; narrower
+// code fits the cache and the barrier only costs: n=17 1244 -> 1169).
+#ifndef TSNMF_WL_SYNC
+#define TSNMF_WL_SYNC 4
+#endif
+constexpr int wl_sync(int n) { return n >= 24 ? TSNMF_WL_SYNC : 0; }
+
 template <int N, int S>
-__global__ void __launch_bounds__(32)
-    tsqr_warp_leaf_kernel(const double* __restrict__ x, int64_t m, int64_t ldx, int64_t rows_per_warp, WlGeom g,
-                          double* __restrict__ slots, double* __restrict__ stats) {
+__global__ void __launch_bounds__(256)
+    tsqr_warp_leaf_kernel(const double* __restrict__ x, int64_t m, int64_t ldx, int64_t rows_per_warp, int nleaves,
+                          WlGeom g, double* __restrict__ slots, double* __restrict__ stats) {
   extern __shared__ __align__(16) double smem[];
   constexpr int BR = 32 * S;
-  const int lane = threadIdx.x;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int ls = g.ls, pld = g.pld;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
-  double* stg = smem + g.stage_off;
-  double* P = smem + g.prod_off;
-  double* Rs = smem + g.r_off;  // R(i, c) at Rs[i * N + c]
-  double* TW = smem + g.tw_off;
-  const int64_t leaf = blockIdx.x;
+  double* base = smem + (size_t)wib * g.total;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base);
+  double* stg = base + g.stage_off;
+  double* P = base + g.prod_off;
+  double* Rs = base + g.r_off;  // R(i, c) at Rs[i * N + c]
+  double* TW = base + g.tw_off;
+  const int64_t leaf = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;  // surplus warps (leaf >= nleaves) idle
   const int64_t rbeg = leaf * rows_per_warp;
   const int64_t rend = min64(m, rbeg + rows_per_warp);
+  const int64_t nblk = rows_per_warp / BR;
+  constexpr int kWlSync = wl_sync(N);
   for (int i = lane; i < N * N; i += 32) Rs[i] = 0.0;
   for (int i = lane; i < N + 1; i += 32) TW[i] = 0.0;
   if (lane == 0) {
@@ -923,14 +939,25 @@ __global__ void __launch_bounds__(32)
   };
   double l1 = 0.0, sq = 0.0;  // lane c: column c
   unsigned phase = 0;
-  bool bulk = rbeg < rend ? issue(rbeg, (int)min64(BR, rend - rbeg)) : false;
-  for (int64_t r0 = rbeg; r0 < rend; r0 += BR) {
-    const int cnt = (int)min64(BR, rend - r0);
-    if (bulk) {
-      mbar_wait_parity(bar, phase);
-      phase ^= 1u;
-    } else {
-      cp_async_wait<0>();
+  // every warp runs nblk blocks (empty ones past its rows) so CTA barriers stay matched
+  auto count_of = [&](int64_t b) -> int { return (int)max64(0, min64(BR, rend - (rbeg + b * BR))); };
+  bool bulk = false, pending = false;
+  if (count_of(0) > 0) {
+    bulk = issue(rbeg, count_of(0));
+    pending = true;
+  }
+  for (int64_t b = 0; b < nblk; ++b) {
+    const int64_t r0 = rbeg + b * BR;
+    const int cnt = count_of(b);
+    if (kWlSync == 0 && cnt == 0) break;
+    if (pending) {
+      if (bulk) {
+        mbar_wait_parity(bar, phase);
+        phase ^= 1u;
+      } else {
+        cp_async_wait<0>();
+      }
+      pending = false;
     }
     __syncwarp();
     double xr[S][N];
@@ -959,7 +986,10 @@ __global__ void __launch_bounds__(32)
       sq += q0 + q1;
     }
     __syncwarp();  // the whole warp is done reading the stage buffer
-    if (r0 + BR < rend) bulk = issue(r0 + BR, (int)min64(BR, rend - r0 - BR));
+    if (b + 1 < nblk && count_of(b + 1) > 0) {
+      bulk = issue(r0 + BR, count_of(b + 1));
+      pending = true;
+    }
     // Column steps, straight-line code (N, j, c compile-time; no branches): lane c (j < c < N) owns
     // w_c = R(j, c) + sum over the block of v x[:, c].  Column j+1 is updated first; the remaining
     // columns' updates of step j are deferred into step j+1, behind its norm butterfly.
@@ -968,8 +998,16 @@ __global__ void __launch_bounds__(32)
     for (int q = 0; q < S; ++q) v_prev[q] = 0.0;
 #pragma unroll
     for (int j = 0; j < N; ++j) {
-      // R row j is only changed by reflector j, so R(j, c) is read up front (off the chain)
-      const double rjc = Rs[j * N + (lane < N ? lane : 0)];
+      if (kWlSync > 0 && j % (kWlSync > 0 ? kWlSync : 1) == 0) named_sync(1, blockDim.x);
+      // Column sums of the product tile: the V = N-1-j live columns are covered by L = pow2ceil(V) lanes,
+      // and the 32 rows split over the 32/L lane groups (L rows each), combined by a shuffle butterfly —
+      // L loads per lane instead of 32.  Lane l: column j+1+(l % L), rows (l / L)*L ...
+      const int L = pow2ceil(N - 1 - j);
+      const int col = j + 1 + (lane & (L - 1));
+      const int grow = (lane & ~(L - 1)) & 31;
+      // R row j is only changed by reflector j, so R(j, .) is read up front (off the chain)
+      const double rjc = Rs[j * N + (col < N ? col : N - 1)];
+      const double alpha = Rs[j * N + j];
       double d = 0.0;
 #pragma unroll
       for (int q = 0; q < S; ++q) d = fma(xr[q][j], xr[q][j], d);
@@ -995,7 +1033,6 @@ __global__ void __launch_bounds__(32)
           }
         }
       }
-      const double alpha = __shfl_sync(0xffffffffu, rjc, j);
       const bool live = d > 0.0;
       const double ss = live ? fma(alpha, alpha, d) : 1.0;
       const double inv = rsqrt_nb(ss);
@@ -1031,19 +1068,17 @@ __global__ void __launch_bounds__(32)
             prow[c] = p0;
         }
         __syncwarp();
-        // every lane sums its column of the tile (lanes outside (j, N) read bytes they then discard)
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        // lanes whose column is >= N sum bytes they then discard (inside the CTA's shared memory)
+        double sa[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-        for (int row = 0; row < 32; row += 4) {
-          s0 += P[(row + 0) * pld + lane];
-          s1 += P[(row + 1) * pld + lane];
-          s2 += P[(row + 2) * pld + lane];
-          s3 += P[(row + 3) * pld + lane];
-        }
-        const double tw = tau * (rjc + ((s0 + s1) + (s2 + s3)));
-        if (lane > j && lane < N) {
-          Rs[j * N + lane] = rjc - tw;
-          TW[lane] = tw;
+        for (int r = 0; r < L; ++r) sa[r & 3] += P[(grow + r) * pld + col];
+        double sum = (sa[0] + sa[1]) + (sa[2] + sa[3]);
+#pragma unroll
+        for (int o = L; o < 32; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        const double tw = tau * (rjc + sum);
+        if (lane < L && col < N) {
+          Rs[j * N + col] = rjc - tw;
+          TW[col] = tw;
         }
       }
       if (lane == j) Rs[j * N + j] = beta;
@@ -1059,6 +1094,7 @@ __global__ void __launch_bounds__(32)
     }
   }
   __syncwarp();
+  if (leaf >= nleaves) return;
   double* R = slots + leaf * g.npad * g.npad;
   if (lane < g.npad) {
     for (int i = 0; i < g.npad; ++i)
@@ -1255,11 +1291,11 @@ WlGeom warp_leaf_geom(int n, int S) {
   g.total = g.tw_off + (int)round_up(n + 1, 2);
   return g;
 }
-// resident warp leaves per SM: shared memory (228 KB per SM, 1 KB reserved per CTA) and registers
-// (<= 255 per thread -> 8 one-warp CTAs)
+// warp leaves per CTA (one CTA per SM): shared memory (227 KB per CTA) and registers (<= 255 per thread
+// -> 8 warps)
 int warp_leaf_per_sm(const WlGeom& g) {
-  const int bytes = (int)sizeof(double) * g.total + 1024;
-  int k = (228 * 1024) / bytes;
+  const int bytes = (int)sizeof(double) * g.total;
+  int k = (227 * 1024) / bytes;
   return k < 1 ? 1 : (k > 8 ? 8 : k);
 }
 void warp_leaf_plan(int n, int64_t m, int* nleaves, int64_t* rows_per_warp) {
@@ -1321,11 +1357,13 @@ int warp_leaf_launch(const double* x, int64_t m, int64_t ldx, int64_t rpw, int n
                      cudaStream_t st) {
   constexpr int S = warp_leaf_s_of(N);
   const WlGeom g = warp_leaf_geom(N, S);
-  const int bytes = (int)sizeof(double) * g.total;
+  const int w = warp_leaf_per_sm(g);
+  const int bytes = (int)sizeof(double) * g.total * w;
   TSNMF_CUDA_CHECK(
       cudaFuncSetAttribute(tsqr_warp_leaf_kernel<N, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   prof_mark(kProfTsqrLeaf, true, st);
-  tsqr_warp_leaf_kernel<N, S><<<nleaves, 32, bytes, st>>>(x, m, ldx, rpw, g, slots, stats);
+  tsqr_warp_leaf_kernel<N, S><<<(unsigned)ceil_div(nleaves, w), 32 * w, bytes, st>>>(x, m, ldx, rpw, nleaves, g,
+                                                                                      slots, stats);
   TSNMF_LAUNCH_CHECK();
   prof_mark(kProfTsqrLeaf, false, st);
   return small_tree<(N <= 8 ? 8 : (N + 3) / 4 * 4)>(N, nleaves, g.npad, slots, st);
