@@ -937,7 +937,10 @@ __global__ void __launch_bounds__(256)
     cp_async_commit();
     return false;
   };
-  double l1 = 0.0, sq = 0.0;  // lane c: column c
+  // column stats: 32/N lanes per column (row phases), combined through shared memory at the end
+  constexpr int kStatPhases = 32 / N;
+  const int scol = lane % N, sph = lane / N;
+  double l1 = 0.0, sq = 0.0;
   unsigned phase = 0;
   // every warp runs nblk blocks (empty ones past its rows) so CTA barriers stay matched
   auto count_of = [&](int64_t b) -> int { return (int)max64(0, min64(BR, rend - (rbeg + b * BR))); };
@@ -967,18 +970,18 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
       for (int c = 0; c < N; ++c) xr[q][c] = row < cnt ? stg[row * ls + c] : 0.0;
     }
-    if (stats && lane < N) {
+    if (stats && sph < kStatPhases) {  // lane: column scol, rows sph, sph + phases, ...
       double a0 = 0.0, a1 = 0.0, q0 = 0.0, q1 = 0.0;
-      int row = 0;
-      for (; row + 2 <= cnt; row += 2) {
-        const double v0 = stg[row * ls + lane], v1 = stg[(row + 1) * ls + lane];
+      int row = sph;
+      for (; row + kStatPhases < cnt; row += 2 * kStatPhases) {
+        const double v0 = stg[row * ls + scol], v1 = stg[(row + kStatPhases) * ls + scol];
         a0 += fabs(v0);
         a1 += fabs(v1);
         q0 = fma(v0, v0, q0);
         q1 = fma(v1, v1, q1);
       }
       if (row < cnt) {
-        const double v0 = stg[row * ls + lane];
+        const double v0 = stg[row * ls + scol];
         a0 += fabs(v0);
         q0 = fma(v0, v0, q0);
       }
@@ -1095,13 +1098,22 @@ __global__ void __launch_bounds__(256)
   }
   __syncwarp();
   if (leaf >= nleaves) return;
+  P[lane] = l1;
+  P[32 + lane] = sq;
+  __syncwarp();
   double* R = slots + leaf * g.npad * g.npad;
   if (lane < g.npad) {
     for (int i = 0; i < g.npad; ++i)
       R[(int64_t)i * g.npad + lane] = (i < N && lane < N && i <= lane) ? Rs[i * N + lane] : 0.0;
     if (stats) {
-      stats[leaf * 2 * g.npad + lane] = lane < N ? l1 : 0.0;
-      stats[leaf * 2 * g.npad + g.npad + lane] = lane < N ? sq : 0.0;
+      double a = 0.0, q = 0.0;
+      if (lane < N)
+        for (int k = 0; k < kStatPhases; ++k) {
+          a += P[k * N + lane];
+          q += P[32 + k * N + lane];
+        }
+      stats[leaf * 2 * g.npad + lane] = a;
+      stats[leaf * 2 * g.npad + g.npad + lane] = q;
     }
   }
 }
