@@ -96,17 +96,43 @@ __device__ long long g_trace[8][64 * 64];
 #endif
 constexpr bool kPairLookahead = TSNMF_PAIR_LOOKAHEAD != 0;  // panel warp joins the helper's lookahead
 
-// 1/sqrt(a) and 1/a for the Householder scalars: hardware approximation + Newton steps (each doubles the
-// correct bits: ~23 -> ~46 -> full), accurate to ~1 ulp; outside [2^-900, 2^900] (where the .ftz
-// approximation would flush) the IEEE library versions are used.  a > 0 here.
+__host__ __device__ constexpr int pow2ceil(int v) {  // v <= 32
+  return v <= 1 ? 1 : (v <= 2 ? 2 : (v <= 4 ? 4 : (v <= 8 ? 8 : (v <= 16 ? 16 : 32))));
+}
+
+// 1/sqrt(a), 1/a for the Householder scalars (a > 0, any finite magnitude incl. subnormal) without
+// branches: the argument is scaled by an even power of two into the range where the .ftz approximation +
+// two Newton steps is accurate (~1 ulp), and the result scaled back exactly.  Branch-free so a column step
+// stays one basic block and the scheduler can overlap off-chain work with the scalar chain.
+__device__ __forceinline__ double rsqrt_nb(double a) {
+  const double sc = a < 0x1p-900 ? 0x1p+600 : (a > 0x1p+900 ? 0x1p-600 : 1.0);
+  const double as = a * sc * sc;
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(as));
+  const double h = 0.5 * as;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return y * sc;
+}
+__device__ __forceinline__ double rcp_nb(double a) {
+  const double sc = a < 0x1p-900 ? 0x1p+600 : (a > 0x1p+900 ? 0x1p-600 : 1.0);
+  const double as = a * sc;
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(as));
+  y = y * fma(-as, y, 2.0);
+  y = y * fma(-as, y, 2.0);
+  return y * sc;
+}
+
+// Branchy variants (range test beside the Newton chain, IEEE path almost never taken): fewer instructions
+// and registers than the branch-free ones, which the register-capped two-CTA panel build prefers.
 __device__ __forceinline__ double fast_rsqrt(double a) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
   const double h = 0.5 * a;
   y = y * fma(-h * y, y, 1.5);
   y = y * fma(-h * y, y, 1.5);
-  // the range test runs beside the Newton chain (not in front of it); the branch is almost never taken
-  if (!(a > 0x1p-900 && a < 0x1p+900)) y = rsqrt(a);  // denormal / extreme range: IEEE path
+  if (!(a > 0x1p-900 && a < 0x1p+900)) y = rsqrt(a);
   return y;
 }
 __device__ __forceinline__ double fast_rcp(double a) {
@@ -183,15 +209,32 @@ __device__ __forceinline__ void panel_factor_lazy(double* __restrict__ Bs, int l
       d[js - 1] *= scale_prev;
     }
     // (C) reflector scalars
+    // (branch-free: the whole column step is one basic block, so the off-chain work of (E) can be
+    // scheduled into the latency of this chain)
+    // (measured: C2 n=200 228 -> 234 GB/s; the register-capped two-CTA build (kPreload false, n <= 64) is
+    // faster with the branch, 352 vs 339 GB/s at n=64)
     const double alpha = kPreload ? ralpha[js] : Rd[js * kNB + js];
-    double tau = 0.0, scale = 0.0, beta = alpha;
-    if (d[js] > 0.0) {
-      const double ss = fma(alpha, alpha, d[js]);
-      const double inv = fast_rsqrt(ss);
+    double tau, scale, beta;
+    if constexpr (kPreload) {
+      const bool live = d[js] > 0.0;
+      const double ss = live ? fma(alpha, alpha, d[js]) : 1.0;
+      const double inv = rsqrt_nb(ss);
       const double nrm = ss * inv;
-      beta = -copysign(nrm, alpha);
-      tau = fma(fabs(alpha), inv, 1.0);
-      scale = copysign(fast_rcp(fabs(alpha) + nrm), alpha);
+      beta = live ? -copysign(nrm, alpha) : alpha;
+      tau = live ? fma(fabs(alpha), inv, 1.0) : 0.0;
+      scale = live ? copysign(rcp_nb(fabs(alpha) + nrm), alpha) : 0.0;
+    } else {
+      tau = 0.0;
+      scale = 0.0;
+      beta = alpha;
+      if (d[js] > 0.0) {
+        const double ss = fma(alpha, alpha, d[js]);
+        const double inv = fast_rsqrt(ss);
+        const double nrm = ss * inv;
+        beta = -copysign(nrm, alpha);
+        tau = fma(fabs(alpha), inv, 1.0);
+        scale = copysign(fast_rcp(fabs(alpha) + nrm), alpha);
+      }
     }
     // (D) critical: next pivot's factor, eager update of the next pivot column, next step's dots
     if (js + 1 < kNB) {
@@ -748,11 +791,11 @@ __device__ __forceinline__ void small_fold_block(const double* __restrict__ src,
     double tau = 0.0, scale = 0.0, beta = alpha;
     if (d > 0.0) {
       const double ss = fma(alpha, alpha, d);
-      const double inv = fast_rsqrt(ss);
+      const double inv = rsqrt_nb(ss);
       const double nrm = ss * inv;
       beta = -copysign(nrm, alpha);
       tau = fma(fabs(alpha), inv, 1.0);
-      scale = copysign(fast_rcp(fabs(alpha) + nrm), alpha);
+      scale = copysign(rcp_nb(fabs(alpha) + nrm), alpha);
     }
     const double v = xr[j] * scale;
     __syncwarp();  // every lane has read the previous column's tw values from buf
@@ -859,32 +902,6 @@ struct WlGeom {
   int total;     // doubles
 };
 
-// 1/sqrt(a), 1/a (a > 0, any finite magnitude incl. subnormal) without branches: the argument is scaled
-// by an even power of two into the range where the .ftz approximation + two Newton steps is accurate
-// (~1 ulp), and the result scaled back exactly.  Branch-free so the column step stays one basic block.
-__host__ __device__ constexpr int pow2ceil(int v) {  // v <= 32
-  return v <= 1 ? 1 : (v <= 2 ? 2 : (v <= 4 ? 4 : (v <= 8 ? 8 : (v <= 16 ? 16 : 32))));
-}
-
-__device__ __forceinline__ double rsqrt_nb(double a) {
-  const double sc = a < 0x1p-900 ? 0x1p+600 : (a > 0x1p+900 ? 0x1p-600 : 1.0);
-  const double as = a * sc * sc;
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(as));
-  const double h = 0.5 * as;
-  y = y * fma(-h * y, y, 1.5);
-  y = y * fma(-h * y, y, 1.5);
-  return y * sc;
-}
-__device__ __forceinline__ double rcp_nb(double a) {
-  const double sc = a < 0x1p-900 ? 0x1p+600 : (a > 0x1p+900 ? 0x1p-600 : 1.0);
-  const double as = a * sc;
-  double y;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(as));
-  y = y * fma(-as, y, 2.0);
-  y = y * fma(-as, y, 2.0);
-  return y * sc;
-}
 
 // CTA barrier every wl_sync(N) column steps (0: none).  The warps of a CTA run the same straight-line
 // column code; for wide blocks (N >= 24: ~150 KB of code per block fold) keeping them within a few columns
