@@ -28,6 +28,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FP64_PEAK_TFLOPS = 37.0  # measured DMMA peak, profiles/r01_peaks.json (no FP64 entry in MEASURED_PEAKS.json)
+FP64_FMA_PEAK_TFLOPS = 34.2  # measured DFMA peak (same file): the narrow warp-leaf TSQR runs on the FMA pipe
 METRIC = "1-pass TSQR/Gram GB/s of X and % of HBM peak at 1/2/4/8 B200 vs CPU ref"
 
 
@@ -351,7 +352,11 @@ def main():
     leaf_flops = 2.0 * n * n * (hi - lo)
     leaf_tf = leaf_flops / (leaf_ms * 1e-3) / 1e12
     plan = dv.tsqr_plan(n, hi - lo)
-    tpr = ncu_traffic_per_row(os.path.join(ROOT, "profiles", "r01_tsqr_leaf_ncu_full.txt"), 1 << 21)
+    narrow = plan["panel"] == 1  # n <= 32: register-block warp leaf (FP64 FMA), else the DMMA panel leaf
+    prof_file, prof_rows = (("r01_tsqr_warp_leaf_ncu_full.txt", 1 << 22) if narrow
+                            else ("r01_tsqr_leaf_ncu_full.txt", 1 << 21))
+    tpr = ncu_traffic_per_row(os.path.join(ROOT, "profiles", prof_file), prof_rows)
+    peak_tf = FP64_FMA_PEAK_TFLOPS if narrow else FP64_PEAK_TFLOPS
 
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
@@ -363,15 +368,17 @@ def main():
                    "resident_gb_per_gpu": round(bytes_local / 1e9, 2), "parallelism": f"rows{world}",
                    "l2": "inputs (>=13 GB per GPU) exceed the 126 MB L2; no flush needed",
                    "tsqr_plan": plan},
-        "roofline": {"bound": "tensor", "achieved": leaf_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                     "frac": leaf_tf / FP64_PEAK_TFLOPS,
+        "roofline": {"bound": "tensor", "achieved": leaf_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                     "frac": leaf_tf / peak_tf,
                      "traffic": tpr * (hi - lo) if tpr else None,
-                     "traffic_source": "ncu --set full dram__bytes_read+write of tsqr_leaf_kernel at m=2^21 "
-                                       "(profiles/r01_tsqr_leaf_ncu_full.txt), per row x rows per launch; "
+                     "traffic_source": f"ncu --set full dram__bytes_read+write of the leaf at m={prof_rows} "
+                                       f"(profiles/{prof_file}), per row x rows per launch; "
                                        f"algorithmic {8 * n * (hi - lo)} B",
-                     "kernel": "tsqr_leaf_kernel (FP64 DMMA m8n8k4)",
+                     "kernel": ("tsqr_warp_leaf_kernel (FP64 FMA, one Householder chain per warp)" if narrow
+                                else "tsqr_leaf_kernel (FP64 DMMA m8n8k4)"),
                      "algorithmic": f"2 n^2 = {2 * n * n} flop per row x {hi - lo} rows per launch",
-                     "peak_source": "measured FP64 DMMA peak, profiles/r01_peaks.json",
+                     "peak_source": ("measured FP64 DFMA peak" if narrow else "measured FP64 DMMA peak")
+                                    + ", profiles/r01_peaks.json",
                      "kernel_ms": leaf_ms, "share_of_step": leaf_ms / ms,
                      "hbm_gbs": bytes_local / (leaf_ms * 1e-3) / 1e9,
                      "hbm_frac": bytes_local / (leaf_ms * 1e-3) / 1e9 / hbm, "hbm_peak": hbm,

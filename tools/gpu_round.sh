@@ -20,4 +20,9 @@ python tools/run_kernel.py gram 4194304 200 1 > gpurun_out/plain_g.log 2>&1 && \
 python tools/run_kernel.py sketch 1048576 200 1 > gpurun_out/plain_s.log 2>&1 && \
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:sketch_gemm -c 1 -o gpurun_out/skgemm_full \
   python tools/run_kernel.py sketch 1048576 200 1 > gpurun_out/ncu_full_s.log 2>&1
+python tools/run_kernel.py tsqr 4194304 25 1 > gpurun_out/plain_n25.log 2>&1 && \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:warp_leaf -c 1 -o gpurun_out/tsqr_warp_leaf_full \
+  python tools/run_kernel.py tsqr 4194304 25 1 > gpurun_out/ncu_full_wl.log 2>&1
+timeout 900 python bench.py --config C4 --rows 400000000 --steps 3 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_C4.log 2>&1
+timeout 900 python bench.py --config C5 --steps 3 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_C5.log 2>&1
 echo done

@@ -48,6 +48,8 @@ if os.path.exists(os.path.join(g, "launches.csv")):
 for rep, name, desc in [("tsqr_leaf_full.ncu-rep", "tsqr_leaf", "tsqr_leaf_kernel on 2^21 x 200 (tools/run_kernel.py tsqr 2097152 200 1)"),
                         ("gram_full2.ncu-rep", "gram", "gram_kernel on 2^22 x 200 (tools/run_kernel.py gram 4194304 200 1)"),
                         ("skgemm_full.ncu-rep", "sketch_gemm", "sketch_gemm_kernel on 2^20 x 200, k=400"),
+                        ("tsqr_warp_leaf_full.ncu-rep", "tsqr_warp_leaf",
+                         "tsqr_warp_leaf_kernel<25,3> on 2^22 x 25 (C4 width; tools/run_kernel.py tsqr 4194304 25 1)"),
                         ("tsqr_small_full.ncu-rep", "tsqr_small_leaf",
                          "tsqr_small_leaf_kernel<28> on 2^22 x 25 (C4 width; tools/run_kernel.py tsqr 4194304 25 1)")]:
     if os.path.exists(os.path.join(g, rep)):
