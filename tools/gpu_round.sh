@@ -25,4 +25,8 @@ python tools/run_kernel.py tsqr 4194304 25 1 > gpurun_out/plain_n25.log 2>&1 && 
   python tools/run_kernel.py tsqr 4194304 25 1 > gpurun_out/ncu_full_wl.log 2>&1
 timeout 900 python bench.py --config C4 --rows 400000000 --steps 3 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_C4.log 2>&1
 timeout 900 python bench.py --config C5 --steps 3 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_C5.log 2>&1
+# summarise on the box (the .ncu-rep files exceed gpurun's 64 MiB copy-back limit)
+TSNMF_PROFILE_OUT=gpurun_out/profiles_out python tools/summarize_profiles.py r01 > gpurun_out/summarize.log 2>&1
+mkdir -p gpurun_out/reps_keep && mv gpurun_out/tsqr_warp_leaf_full.ncu-rep gpurun_out/reps_keep/ 2>/dev/null
+rm -f gpurun_out/*.ncu-rep
 echo done

@@ -2,7 +2,8 @@
 import collections, csv, json, os, subprocess, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
-out_dir = os.path.join(ROOT, "profiles")
+out_dir = os.environ.get("TSNMF_PROFILE_OUT") or os.path.join(ROOT, "profiles")
+os.makedirs(out_dir, exist_ok=True)
 g = os.path.join(ROOT, "gpurun_out")
 
 def launches():
