@@ -177,6 +177,32 @@ __host__ __device__ __forceinline__ int smem_stride(int cols) {
   return s;
 }
 
+// 1/sqrt(a), 1/a for the Householder scalars (a > 0, any finite magnitude incl. subnormal) without
+// branches: the argument is scaled by an even power of two into the range where the .ftz approximation +
+// two Newton steps is accurate (<= 2 ulp vs IEEE, tools/probe_rsqrt.cu), and the result scaled back
+// exactly.  Branch-free so a column step stays one basic block and the scheduler can overlap off-chain
+// work with the scalar chain.  (A single third-order correction step instead of two Newton steps, with
+// the range-scaled copy computed beside the chain, measured no faster and spills in the narrow kernels.)
+__device__ __forceinline__ double rsqrt_nb(double a) {
+  const double sc = a < 0x1p-900 ? 0x1p+600 : (a > 0x1p+900 ? 0x1p-600 : 1.0);
+  const double as = a * sc * sc;
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(as));
+  const double h = 0.5 * as;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return y * sc;
+}
+__device__ __forceinline__ double rcp_nb(double a) {
+  const double sc = a < 0x1p-900 ? 0x1p+600 : (a > 0x1p+900 ? 0x1p-600 : 1.0);
+  const double as = a * sc;
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(as));
+  y = y * fma(-as, y, 2.0);
+  y = y * fma(-as, y, 2.0);
+  return y * sc;
+}
+
 // cp.async helpers (LDGSTS): global -> shared without staging through registers.
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);

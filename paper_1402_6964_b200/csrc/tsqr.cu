@@ -100,29 +100,6 @@ __host__ __device__ constexpr int pow2ceil(int v) {  // v <= 32
   return v <= 1 ? 1 : (v <= 2 ? 2 : (v <= 4 ? 4 : (v <= 8 ? 8 : (v <= 16 ? 16 : 32))));
 }
 
-// 1/sqrt(a), 1/a for the Householder scalars (a > 0, any finite magnitude incl. subnormal) without
-// branches: the argument is scaled by an even power of two into the range where the .ftz approximation +
-// two Newton steps is accurate (~1 ulp), and the result scaled back exactly.  Branch-free so a column step
-// stays one basic block and the scheduler can overlap off-chain work with the scalar chain.
-__device__ __forceinline__ double rsqrt_nb(double a) {
-  const double sc = a < 0x1p-900 ? 0x1p+600 : (a > 0x1p+900 ? 0x1p-600 : 1.0);
-  const double as = a * sc * sc;
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(as));
-  const double h = 0.5 * as;
-  y = y * fma(-h * y, y, 1.5);
-  y = y * fma(-h * y, y, 1.5);
-  return y * sc;
-}
-__device__ __forceinline__ double rcp_nb(double a) {
-  const double sc = a < 0x1p-900 ? 0x1p+600 : (a > 0x1p+900 ? 0x1p-600 : 1.0);
-  const double as = a * sc;
-  double y;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(as));
-  y = y * fma(-as, y, 2.0);
-  y = y * fma(-as, y, 2.0);
-  return y * sc;
-}
 
 // Branchy variants (range test beside the Newton chain, IEEE path almost never taken): fewer instructions
 // and registers than the branch-free ones, which the register-capped two-CTA panel build prefers.
@@ -791,11 +768,11 @@ __device__ __forceinline__ void small_fold_block(const double* __restrict__ src,
     double tau = 0.0, scale = 0.0, beta = alpha;
     if (d > 0.0) {
       const double ss = fma(alpha, alpha, d);
-      const double inv = rsqrt_nb(ss);
+      const double inv = fast_rsqrt(ss);
       const double nrm = ss * inv;
       beta = -copysign(nrm, alpha);
       tau = fma(fabs(alpha), inv, 1.0);
-      scale = copysign(rcp_nb(fabs(alpha) + nrm), alpha);
+      scale = copysign(fast_rcp(fabs(alpha) + nrm), alpha);
     }
     const double v = xr[j] * scale;
     __syncwarp();  // every lane has read the previous column's tw values from buf
