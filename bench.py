@@ -63,7 +63,8 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="C2")
     p.add_argument("--rows", type=int, default=None, help="override total rows m")
-    p.add_argument("--k", type=int, default=400, help="sketch rows for the GX pass")
+    p.add_argument("--k", type=int, default=None, help="sketch rows for the GX pass (default: the config's, "
+                                                         "k=128 for C5, 400 otherwise)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-extra", action="store_true", help="skip the Gram / GX passes")
@@ -274,6 +275,8 @@ def main():
         dist.init_process_group("nccl", device_id=devc)
     lib = _native.load()
 
+    if args.k is None:
+        args.k = 128 if args.config == "C5" else 400
     spec = synthetic.config(args.config)
     if args.rows:
         spec = synthetic.config(args.config, m=args.rows)

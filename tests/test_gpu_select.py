@@ -98,3 +98,40 @@ def test_xray_device_usage_errors():
         tb.xray_greedy(np.random.default_rng(1).uniform(0, 1, (80, 80)), dv.nnls_max_cols() + 1, device=True)
     with pytest.raises(UsageError):
         tb.xray_greedy(m, 9, device=True)
+
+
+# ---------------------------------------------------------------------------
+# Every BASELINE config's generator at a reduced row count (the full sizes are bench lines, checked by
+# size-independent properties in test_gpu_fullsize.py): the device pass, selection and coefficients
+# against the oracle's restatement of the reference pass on the same X.
+
+
+@pytest.mark.parametrize("name,sigma,k", [("C2", None, 400), ("C3", 1e-2, 0), ("C4", None, 0), ("C5", None, 128)])
+def test_config_reduced_rows_selection_matches_oracle(oracle, name, sigma, k):
+    m = 1 << 17
+    ospec = oracle.config_spec(name, m=m, sigma=sigma)
+    x = oracle.config_rows(ospec, 0, m)
+    res = tb.stream_pass([tb.RowChunk(0, dv.torch().from_numpy(x).cuda())], sketch_rows=k or None, seed=0)
+    ref = oracle.stream_pass(oracle.chunks_of(x, 8192), sketch_rows=k or None, seed=0)
+    r_dev, r_ref = res.factor.entries, ref.r
+    assert np.linalg.norm(r_dev - r_ref) <= 1e-10 * np.linalg.norm(r_ref)
+    np.testing.assert_allclose(res.stats.l1, ref.l1, rtol=1e-12)
+    if k:
+        assert np.linalg.norm(res.sketch.entries - ref.sketch) <= 1e-12 * np.linalg.norm(ref.sketch)
+    r = ospec.r
+    red_dev = tb.rsvd(res.factor)
+    red_ref = tb.rsvd(tb.TriangularFactor(r_ref))
+    stats_ref = tb.ColumnStats(np.array(ref.l1), np.sqrt(ref.sumsq))
+    k_dev = tb.spa(red_dev, r, normalize=True, stats=res.stats)
+    k_ref = tb.spa(red_ref, r, normalize=True, stats=stats_ref)
+    assert list(k_dev.indices) == list(k_ref.indices)
+    h_dev = tb.compute_h(red_dev, k_dev, device=True)
+    h_ref = tb.compute_h(red_ref, k_ref)
+    assert np.abs(h_dev.entries - h_ref.entries).max() <= H_TOL
+    kx_dev = tb.xray_greedy(red_dev, r, device=True)
+    try:
+        kx_ref = tb.xray_greedy(red_ref, r)
+    except tb.NumericalError:  # the host Lawson-Hanson can cycle at the tolerance
+        kx_ref = None
+    if kx_ref is not None:
+        assert list(kx_dev.indices) == list(kx_ref.indices)
