@@ -28,7 +28,7 @@ from typing import Iterable
 import numpy as np
 
 from . import device as dv
-from .errors import DataError, UsageError
+from .errors import DataError, NumericalError, UsageError
 from .rowchunk import RowChunk
 
 COMBINE_ORDERS = ("tree", "sequential", "first-come")
@@ -474,6 +474,18 @@ def _run_pass(chunks, engine: _PassEngine, combine_order: str):
     return node, n_chunks, depth
 
 
+def _check_square_range(l1: np.ndarray, sq: np.ndarray, stage: str) -> None:
+    """The device kernels form sums of squares without LAPACK's dnrm2-style rescaling, so finite columns
+    whose squares overflow (|x| >~ 1e154) or all underflow (|x| <~ 1e-154) cannot be factored faithfully;
+    report them instead of returning a wrong factor.  (Known divergence: the reference's LAPACK path
+    handles such magnitudes.)  Non-finite data keeps the reference's behaviour (not flagged here)."""
+    bad = np.isfinite(l1) & (~np.isfinite(sq) | ((l1 > 0) & (sq == 0)))
+    if bad.any():
+        j = int(np.flatnonzero(bad)[0])
+        raise NumericalError(f"column {j}: magnitudes outside the range where fp64 squares are representable "
+                             f"(l1 = {l1[j]:.3e}, sum of squares = {sq[j]:.3e}); rescale the data", stage=stage)
+
+
 def stream_pass(chunks: Iterable[RowChunk], *, sketch_rows: int | None = None, seed: int = 0,
                 combine_order: str = "tree", threads: int = 1) -> StreamResult:
     """One traversal of a chunk stream: the triangular factor, the column
@@ -490,7 +502,9 @@ def stream_pass(chunks: Iterable[RowChunk], *, sketch_rows: int | None = None, s
     node, n_chunks, depth = _run_pass(chunks, _PassEngine(True, sketch_rows, seed, False), combine_order)
     if node.rows < node.n:
         raise DataError(f"not tall-and-skinny: m = {node.rows} < n = {node.n}")
-    stats = ColumnStats(l1=node.l1.cpu().numpy(), l2=np.sqrt(node.sq.cpu().numpy()))
+    l1, sq = node.l1.cpu().numpy(), node.sq.cpu().numpy()
+    _check_square_range(l1, sq, "stream_pass")
+    stats = ColumnStats(l1=l1, l2=np.sqrt(sq))
     sk = SketchResult(entries=node.sk.cpu().numpy(), seed=seed) if node.sk is not None else None
     return StreamResult(factor=TriangularFactor(entries=node.r.cpu().numpy()), stats=stats, sketch=sk,
                         rows=node.rows, chunks=n_chunks, tree_depth=depth)
@@ -500,7 +514,9 @@ def gram_pass(chunks: Iterable[RowChunk], *, combine_order: str = "tree") -> Gra
     """NEW: one pass producing X^T X and the column norms (the BASELINE
     north-star Gram variant; no reference function)."""
     node, n_chunks, depth = _run_pass(chunks, _PassEngine(False, None, 0, True), combine_order)
-    stats = ColumnStats(l1=node.l1.cpu().numpy(), l2=np.sqrt(node.sq.cpu().numpy()))
+    l1, sq = node.l1.cpu().numpy(), node.sq.cpu().numpy()
+    _check_square_range(l1, sq, "gram_pass")
+    stats = ColumnStats(l1=l1, l2=np.sqrt(sq))
     return GramResult(gram=node.g.cpu().numpy(), stats=stats, rows=node.rows, chunks=n_chunks, tree_depth=depth)
 
 

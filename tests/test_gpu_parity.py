@@ -368,3 +368,17 @@ def test_device_normals_accuracy_vs_libm(oracle):
     zr = oracle.normal_block(0x48218226FF3CD4BF, 12345, 1 << 20)
     assert np.max(np.abs(z - zr)) <= 4e-15
     np.testing.assert_allclose(z, zr, rtol=1e-12, atol=1e-13)
+
+
+@pytest.mark.parametrize("n", [25, 200])
+def test_magnitude_range(oracle, n):
+    """Scaled data inside the fp64 squared range factors like the oracle (branch-free scalars with exact
+    power-of-two range scaling); outside it the pass reports NumericalError instead of a wrong factor."""
+    x = np.random.default_rng(n).uniform(0, 1, (5000, n))
+    for scale in (1e-120, 1e120):
+        res = tb.stream_pass([tb.RowChunk(0, dev(x * scale))])
+        want = oracle.factor_chunk(x) * scale
+        assert rel_err(res.factor.entries, want) <= R_TOL
+    for scale in (1e-170, 1e170):
+        with pytest.raises(tb.NumericalError):
+            tb.stream_pass([tb.RowChunk(0, dev(x * scale))])

@@ -199,3 +199,19 @@ def test_nnls_input_checks():
     y = nonneg.nnls_solve(np.eye(2), np.array([1.0, -1.0]))
     assert np.array_equal(y, [1.0, 0.0])
     assert extremes.as_matrix(tb.TriangularFactor(np.eye(2))).shape == (2, 2)
+
+
+def test_square_range_check():
+    """Columns whose squares overflow or all underflow are reported (the device kernels do not rescale);
+    zero and non-finite columns are left to the reference's own handling."""
+    import numpy as np
+    import pytest
+
+    from paper_1402_6964_b200.errors import NumericalError
+    from paper_1402_6964_b200.factor import _check_square_range
+
+    _check_square_range(np.array([1.0, 0.0, np.nan]), np.array([1.0, 0.0, np.nan]), "t")
+    with pytest.raises(NumericalError, match="column 1"):
+        _check_square_range(np.array([1.0, 1e-160]), np.array([1.0, 0.0]), "t")
+    with pytest.raises(NumericalError, match="column 0"):
+        _check_square_range(np.array([1e200]), np.array([np.inf]), "t")
