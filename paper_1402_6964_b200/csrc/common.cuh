@@ -142,38 +142,60 @@ __device__ __forceinline__ double bm_log(double u) {
   return fma(de, 0.6931471803691238, fma(de, 1.9082149292705877e-10, 2.0 * sv * p));
 }
 
-// cos(t) for t in [0, 2 pi]: Cody-Waite reduction by pi/2 (two-part constant, k <= 4), Taylor
-// polynomials of cos / sin through r^18 / r^19 on |r| <= pi/4, quadrant select.  Max absolute error
-// ~1.1e-16 vs libm.
-__device__ __forceinline__ double bm_cos(double t) {
-  const int k = __double2int_rn(t * 0.6366197723675814);
+// cos(t) for t = fl(2 pi u2), u2 = w2 2^-53 (the Box-Muller angle): table-driven.  k = round(64 u2) from
+// the integer w2, r = t - k pi/32 (two-part Cody-Waite constant, exact first step), |r| <= pi/64;
+// cos(k pi/32 + r) = C_k cos r - S_k sin r with cos r / sin r through r^8 / r^9 (truncation < 1e-19) and
+// C_k, S_k from a 33-entry table (cos is even: k > 32 uses 64 - k and the sign of the sine term flips).
+// 14 FP64 operations instead of ~26 for the quadrant version (the FP64 pipe is shared with the sketch's
+// DMMAs).  Max absolute error ~2e-16 vs libm.  Table: tools/gen_bm_tables.py.
+// C1 = 0x1.921fb54442e00p-4, C2 = -0x1.cf72cece675d2p-49
+static __device__ const double2 kBmCosTab[33] = {
+    {0x1.0000000000000p+0, 0x0.0p+0},  // k = 0
+    {0x1.fd88da3d12526p-1, 0x1.917a6bc29b42cp-4},  // k = 1
+    {0x1.f6297cff75cb0p-1, 0x1.8f8b83c69a60bp-3},  // k = 2
+    {0x1.e9f4156c62ddap-1, 0x1.294062ed59f06p-2},  // k = 3
+    {0x1.d906bcf328d46p-1, 0x1.87de2a6aea963p-2},  // k = 4
+    {0x1.c38b2f180bdb1p-1, 0x1.e2b5d3806f63bp-2},  // k = 5
+    {0x1.a9b66290ea1a3p-1, 0x1.1c73b39ae68c8p-1},  // k = 6
+    {0x1.8bc806b151741p-1, 0x1.44cf325091dd6p-1},  // k = 7
+    {0x1.6a09e667f3bcdp-1, 0x1.6a09e667f3bcdp-1},  // k = 8
+    {0x1.44cf325091dd6p-1, 0x1.8bc806b151741p-1},  // k = 9
+    {0x1.1c73b39ae68c8p-1, 0x1.a9b66290ea1a3p-1},  // k = 10
+    {0x1.e2b5d3806f63bp-2, 0x1.c38b2f180bdb1p-1},  // k = 11
+    {0x1.87de2a6aea963p-2, 0x1.d906bcf328d46p-1},  // k = 12
+    {0x1.294062ed59f06p-2, 0x1.e9f4156c62ddap-1},  // k = 13
+    {0x1.8f8b83c69a60bp-3, 0x1.f6297cff75cb0p-1},  // k = 14
+    {0x1.917a6bc29b42cp-4, 0x1.fd88da3d12526p-1},  // k = 15
+    {0x0.0p+0, 0x1.0000000000000p+0},  // k = 16
+    {-0x1.917a6bc29b42cp-4, 0x1.fd88da3d12526p-1},  // k = 17
+    {-0x1.8f8b83c69a60bp-3, 0x1.f6297cff75cb0p-1},  // k = 18
+    {-0x1.294062ed59f06p-2, 0x1.e9f4156c62ddap-1},  // k = 19
+    {-0x1.87de2a6aea963p-2, 0x1.d906bcf328d46p-1},  // k = 20
+    {-0x1.e2b5d3806f63bp-2, 0x1.c38b2f180bdb1p-1},  // k = 21
+    {-0x1.1c73b39ae68c8p-1, 0x1.a9b66290ea1a3p-1},  // k = 22
+    {-0x1.44cf325091dd6p-1, 0x1.8bc806b151741p-1},  // k = 23
+    {-0x1.6a09e667f3bcdp-1, 0x1.6a09e667f3bcdp-1},  // k = 24
+    {-0x1.8bc806b151741p-1, 0x1.44cf325091dd6p-1},  // k = 25
+    {-0x1.a9b66290ea1a3p-1, 0x1.1c73b39ae68c8p-1},  // k = 26
+    {-0x1.c38b2f180bdb1p-1, 0x1.e2b5d3806f63bp-2},  // k = 27
+    {-0x1.d906bcf328d46p-1, 0x1.87de2a6aea963p-2},  // k = 28
+    {-0x1.e9f4156c62ddap-1, 0x1.294062ed59f06p-2},  // k = 29
+    {-0x1.f6297cff75cb0p-1, 0x1.8f8b83c69a60bp-3},  // k = 30
+    {-0x1.fd88da3d12526p-1, 0x1.917a6bc29b42cp-4},  // k = 31
+    {-0x1.0000000000000p+0, 0x0.0p+0},  // k = 32
+};
+static __constant__ double kBmCosC[8] = {1.0 / 40320, -1.0 / 720, 1.0 / 24, -0.5,
+                                          1.0 / 362880, -1.0 / 5040, 1.0 / 120, -1.0 / 6};
+__device__ __forceinline__ double bm_cos(double t, uint64_t w2) {
+  const int k = (int)((w2 + (1ull << 46)) >> 47);  // round(64 u2), 0..64
   const double dk = (double)k;
-  const double r = fma(-dk, 6.077100506506192e-11, fma(-dk, 1.5707963267341256, t));
+  const double r = fma(-dk, -0x1.cf72cece675d2p-49, fma(-dk, 0x1.921fb54442e00p-4, t));
+  const double2 cs = __ldg(&kBmCosTab[k <= 32 ? k : 64 - k]);
   const double r2 = r * r;
-  double c = kBmC[20];
-  c = fma(c, r2, kBmC[11]);
-  c = fma(c, r2, kBmC[12]);
-  c = fma(c, r2, kBmC[13]);
-  c = fma(c, r2, kBmC[14]);
-  c = fma(c, r2, kBmC[15]);
-  c = fma(c, r2, kBmC[16]);
-  c = fma(c, r2, kBmC[17]);
-  c = fma(c, r2, kBmC[18]);
-  c = fma(c, r2, kBmC[19]);
-  double sn = kBmC[30];
-  sn = fma(sn, r2, kBmC[21]);
-  sn = fma(sn, r2, kBmC[22]);
-  sn = fma(sn, r2, kBmC[23]);
-  sn = fma(sn, r2, kBmC[24]);
-  sn = fma(sn, r2, kBmC[25]);
-  sn = fma(sn, r2, kBmC[26]);
-  sn = fma(sn, r2, kBmC[27]);
-  sn = fma(sn, r2, kBmC[28]);
-  sn = fma(sn, r2, kBmC[29]);
-  sn *= r;
-  const int q = k & 3;
-  const double v = (q & 1) ? sn : c;
-  return (q == 1 || q == 2) ? -v : v;
+  const double cr = fma(fma(fma(fma(r2, kBmCosC[0], kBmCosC[1]), r2, kBmCosC[2]), r2, kBmCosC[3]), r2, 1.0);
+  const double sp = fma(fma(fma(r2, kBmCosC[4], kBmCosC[5]), r2, kBmCosC[6]), r2, kBmCosC[7]);
+  const double sr = fma(r * r2, sp, r);
+  return fma(k <= 32 ? -cs.y : cs.y, sr, cs.x * cr);
 }
 
 // Standard normal #j: uniforms at counters 2j, 2j+1, Box-Muller cosine branch (_kernels.pyx:49-69):
@@ -182,8 +204,9 @@ __device__ __forceinline__ double bm_cos(double t) {
 // ~250 with the general libdevice versions).  Agreement with the reference's libm: |dz| <= ~1e-15.
 __device__ __forceinline__ double rng_normal(uint64_t stream, uint64_t j) {
   double u1 = __dmul_rn(__dadd_rn((double)(rng_word(stream, 2 * j) >> 11), 0.5), kInv2p53);
-  double u2 = __dmul_rn((double)(rng_word(stream, 2 * j + 1) >> 11), kInv2p53);
-  return __dmul_rn(sqrt(__dmul_rn(-2.0, bm_log(u1))), bm_cos(__dmul_rn(kTwoPi, u2)));
+  const uint64_t w2 = rng_word(stream, 2 * j + 1) >> 11;
+  double u2 = __dmul_rn((double)w2, kInv2p53);
+  return __dmul_rn(sqrt(__dmul_rn(-2.0, bm_log(u1))), bm_cos(__dmul_rn(kTwoPi, u2), w2));
 }
 
 // Single-precision Box-Muller on the same counters (2j, 2j+1), used ONLY by the synthetic-data
