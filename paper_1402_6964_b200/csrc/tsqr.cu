@@ -499,10 +499,9 @@ __device__ __forceinline__ void lookahead_pair(double* __restrict__ Bs, int lds,
 #pragma unroll
   for (int k0 = 0; k0 < 8; k0 += 4)
     dmma(w0, w1, Tm[(k0 + (lane & 3)) * kNB + (lane >> 2)], Wsc[(k0 + (lane & 3)) * 8 + (lane >> 2)]);
-  if (h == 1) {
-    const double2 rv = *reinterpret_cast<const double2*>(rtile);
-    *reinterpret_cast<double2*>(rtile) = make_double2(rv.x - w0, rv.y - w1);
-  }
+  // R_p -= W' from the tile loaded at the start (no second L2 round trip on the lookahead's path: column
+  // block p+1 of R_p is touched by nobody else between the two points)
+  if (h == 1) *reinterpret_cast<double2*>(rtile) = make_double2(rinit.x - w0, rinit.y - w1);
   __syncwarp();
   Wsc[ci] = w0;
   Wsc[ci + 1] = w1;
