@@ -215,3 +215,10 @@ def test_square_range_check():
         _check_square_range(np.array([1.0, 1e-160]), np.array([1.0, 0.0]), "t")
     with pytest.raises(NumericalError, match="column 0"):
         _check_square_range(np.array([1e200]), np.array([np.inf]), "t")
+
+
+def test_default_sketch_rows():
+    """k = ceil(2 r ln max(r, 2)) (reference sketch.py:57-59; values from the live reference)."""
+    from paper_1402_6964_b200.projection import default_sketch_rows
+
+    assert [default_sketch_rows(r) for r in (1, 2, 3, 10, 20, 64)] == [2, 3, 7, 47, 120, 533]
