@@ -27,7 +27,7 @@ namespace tsnmf {
 constexpr int kTqThreads = 256;
 constexpr int kTqWarps = kTqThreads / 32;
 constexpr int kNB = 8;       // panel width (reflectors per compact-WY block)
-constexpr int kMaxRq = 4;    // block rows per lane of each panel warp (block rows <= 256)
+constexpr int kMaxRq = 5;    // block rows per lane of each panel warp (block rows <= 160)
 
 struct TqGeom {
   int n;      // data columns
@@ -1162,7 +1162,11 @@ bool tq_choose(int n, int minb, TqChoice* out) {
   g.lds = smem_stride(g.npad);
   const size_t budget = (minb == 2 ? 113 : 226) * 1024;
   int best = 0;
-  for (int b = 16; b <= 32 * kMaxRq; b += 16) {  // multiple of 16: B -= V W' runs row-block pairs
+  // multiple of 16 (B -= V W' runs row-block pairs; 136 rows at n = 200 with an odd-block tail measured
+  // slower, 228 vs 234 GB/s); above 128 rows (RQ = 5) only for the one-CTA build at n > 64, whose register
+  // budget holds the fifth panel row (n = 128: 160 rows, 249 -> 270 GB/s)
+  const int bmax = (minb == 1 && n > 64) ? 32 * kMaxRq : 128;
+  for (int b = 16; b <= bmax; b += 16) {
     g.brows = b;
     if (TqLayout::bytes(g) <= budget) best = b;
   }
@@ -1234,7 +1238,10 @@ int tq_dispatch_rq(const TqChoice& ch, const double* x, int64_t m, int64_t ldx, 
     case 1: return tq_launch_all<1, MINB>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
     case 2: return tq_launch_all<2, MINB>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
     case 3: return tq_launch_all<3, MINB>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
-    default: return tq_launch_all<4, MINB>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
+    case 4: return tq_launch_all<4, MINB>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
+    default:
+      if constexpr (MINB == 1) return tq_launch_all<5, 1>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
+      return tq_launch_all<4, MINB>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
   }
 }
 
