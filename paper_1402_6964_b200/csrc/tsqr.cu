@@ -556,7 +556,23 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
                           double* __restrict__ stats_out, double* smem) {
   using L = TqLayout;
   constexpr int G = 4;  // column blocks per GEMM group
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
+  int warp = tid >> 5;  // logical warp (role); physical warp = (warp + rot) % 8
+  if constexpr (!kPreload) {
+    // two CTAs per SM: the second CTA's warps usually occupy the next 8 hardware slots, i.e. the same SMSPs
+    // (slot % 4) as the first CTA's, which would put both panel warps and both helpers on SMSP 0.  Rotate
+    // the roles by one warp in that CTA so its latency-critical pair runs on SMSP 1 (a hint only: any
+    // rotation is functionally identical; measured n=64 353 -> 357, n=48 363 -> 371 GB/s; by 2: no change, by 3: -5%).
+    // (broadcast through the reduction scratch, first used long after the block loop's first barrier)
+    volatile int* s_rot = reinterpret_cast<volatile int*>(smem + TqLayout::red(g));
+    if (tid == 0) {
+      unsigned wid;
+      asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+      *s_rot = (int)((wid >> 3) & 1u);
+    }
+    __syncthreads();
+    warp = (warp - *s_rot) & (kTqWarps - 1);
+  }
   const int npad = g.npad, lds = g.lds, brows = g.brows;
   double* Bs = smem;
   double* Rdg = smem + L::rd(g);
