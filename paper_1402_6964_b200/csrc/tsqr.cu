@@ -663,13 +663,18 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
             cbs[gg] = base + kGemmWarps * gg;
             if (cbs[gg] < ncb) ++cnt_g;
           }
+          // a short last group is updated in one call (shared V fragment loads), not block by block
           if (cnt_g == G) {
             update_cbs<G>(Bs, lds, brows, j0, R, npad, Tmc, Wsc, cbs, lane, tq_p);
-          } else {
-            for (int gg = 0; gg < cnt_g; ++gg) {
-              const int one[1] = {cbs[gg]};
-              update_cbs<1>(Bs, lds, brows, j0, R, npad, Tmc, Wsc, one, lane, tq_p);
-            }
+          } else if (cnt_g == 3) {
+            const int three[3] = {cbs[0], cbs[1], cbs[2]};
+            update_cbs<3>(Bs, lds, brows, j0, R, npad, Tmc, Wsc, three, lane, tq_p);
+          } else if (cnt_g == 2) {
+            const int two[2] = {cbs[0], cbs[1]};
+            update_cbs<2>(Bs, lds, brows, j0, R, npad, Tmc, Wsc, two, lane, tq_p);
+          } else if (cnt_g == 1) {
+            const int one[1] = {cbs[0]};
+            update_cbs<1>(Bs, lds, brows, j0, R, npad, Tmc, Wsc, one, lane, tq_p);
           }
         }
       }
