@@ -356,9 +356,10 @@ def main():
     leaf_tf = leaf_flops / (leaf_ms * 1e-3) / 1e12
     plan = dv.tsqr_plan(n, hi - lo)
     narrow = plan["panel"] == 1  # n <= 32: register-block warp leaf (FP64 FMA), else the DMMA panel leaf
-    prof_file, prof_rows = (("r01_tsqr_warp_leaf_ncu_full.txt", 1 << 22) if narrow
-                            else ("r01_tsqr_leaf_ncu_full.txt", 1 << 21))
-    tpr = ncu_traffic_per_row(os.path.join(ROOT, "profiles", prof_file), prof_rows)
+    prof_file, prof_rows, prof_n = (("r01_tsqr_warp_leaf_ncu_full.txt", 1 << 22, 25) if narrow
+                                    else ("r01_tsqr_leaf_ncu_full.txt", 1 << 21, 200))
+    # the committed ncu capture is per width: traffic is only reported for the width it was taken at
+    tpr = ncu_traffic_per_row(os.path.join(ROOT, "profiles", prof_file), prof_rows) if n == prof_n else None
     peak_tf = FP64_FMA_PEAK_TFLOPS if narrow else FP64_PEAK_TFLOPS
 
     line = {
@@ -374,9 +375,10 @@ def main():
         "roofline": {"bound": "tensor", "achieved": leaf_tf, "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": leaf_tf / peak_tf,
                      "traffic": tpr * (hi - lo) if tpr else None,
-                     "traffic_source": f"ncu --set full dram__bytes_read+write of the leaf at m={prof_rows} "
-                                       f"(profiles/{prof_file}), per row x rows per launch; "
-                                       f"algorithmic {8 * n * (hi - lo)} B",
+                     "traffic_source": (f"ncu --set full dram__bytes_read+write of the leaf at m={prof_rows}, "
+                                        f"n={prof_n} (profiles/{prof_file}), per row x rows per launch; "
+                                        f"algorithmic {8 * n * (hi - lo)} B") if tpr else
+                                       f"no committed ncu capture at n={n}",
                      "kernel": ("tsqr_warp_leaf_kernel (FP64 FMA, one Householder chain per warp)" if narrow
                                 else "tsqr_leaf_kernel (FP64 DMMA m8n8k4)"),
                      "algorithmic": f"2 n^2 = {2 * n * n} flop per row x {hi - lo} rows per launch",
