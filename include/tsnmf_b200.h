@@ -87,6 +87,11 @@ int tsnmf_sketch(const double* x, int64_t m, int32_t n, int64_t ldx, int64_t row
 int tsnmf_column_stats(const double* x, int64_t m, int32_t n, int64_t ldx, double* l1, double* sumsq,
                        void* ws, size_t ws_bytes, void* cuda_stream);
 
+/* ---- ingest validation: replaces reference pkg/src/tsnmf/matio.py:81-87 (_check_finite) for device
+ *      batches read by matio.ChunkReader.  *first (device int64) = linear index of the
+ *      first Inf/NaN among x[0 .. count) (row-major), or -1 when all are finite.  x 16-byte aligned. */
+int tsnmf_first_nonfinite(const double* x, int64_t count, int64_t* first, void* cuda_stream);
+
 /* ---- synthetic BASELINE.json configs written straight into device memory: rows
  *      [row0, row0 + rows) of X = max(W [I H'] Pi + sigma N, 0).  mix = [I H'] Pi (r x n, device),
  *      w_kind 0 uniform / 1 lognormal / 2 bumps (bumps: r x 4 x 3 device params, else NULL). */

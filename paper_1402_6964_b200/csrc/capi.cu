@@ -155,6 +155,13 @@ int tsnmf_column_stats(const double* x, int64_t m, int32_t n, int64_t ldx, doubl
   return stats_run(x, m, n, ldx, l1, sumsq, ws, ws_bytes, as_stream(s));
 }
 
+int tsnmf_first_nonfinite(const double* x, int64_t count, int64_t* first, void* s) {
+  if (count < 0) return set_error(kUsage, "first_nonfinite: negative count");
+  if ((count > 0 && !x) || !first) return set_error(kUsage, "first_nonfinite: null pointer");
+  if (reinterpret_cast<uintptr_t>(x) & 15) return set_error(kUsage, "first_nonfinite: x must be 16-byte aligned");
+  return first_nonfinite_run(x, count, first, as_stream(s));
+}
+
 int tsnmf_generate(double* x, int64_t ldx, int64_t row0, int64_t rows, int32_t n, int32_t r, const double* mix,
                    int32_t w_kind, const double* bumps, int64_t m_total, double sigma, uint64_t seed, void* s) {
   if (r < 1 || r > n) return set_error(kUsage, "generate: need 1 <= r <= n, got r=%d, n=%d", r, n);

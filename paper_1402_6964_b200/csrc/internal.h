@@ -40,6 +40,7 @@ int sketch_run(const double* x, int64_t m, int n, int64_t ldx, int64_t row_offse
                cudaStream_t st);
 
 size_t stats_workspace_bytes(int64_t m, int n);
+int first_nonfinite_run(const double* x, int64_t count, int64_t* first, cudaStream_t st);
 int stats_run(const double* x, int64_t m, int n, int64_t ldx, double* l1, double* sumsq, void* ws, size_t ws_bytes,
               cudaStream_t st);
 

@@ -166,4 +166,51 @@ int generate_run(double* x, int64_t ldx, int64_t row0, int64_t rows, int n, int 
   return kOk;
 }
 
+// ---------------------------------------------------------------------------
+// Ingest validation (reference matio.py:81-87 _check_finite): the first non-finite
+// element of a contiguous row-major batch, as a linear index (-1 when all are finite).  HBM-bound:
+// 16-byte loads, one exponent test per element, a warp vote, one atomicMin per warp that saw one.
+__global__ void first_nonfinite_kernel(const double* __restrict__ x, int64_t count,
+                                       unsigned long long* __restrict__ first) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t pairs = count >> 1;
+  const double2* x2 = reinterpret_cast<const double2*>(x);
+  unsigned long long best = ~0ull;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pairs; i += stride) {
+    const double2 v = __ldg(&x2[i]);
+    // exponent all ones <=> Inf or NaN
+    const bool b0 = (__double2hiint(v.x) & 0x7ff00000) == 0x7ff00000;
+    const bool b1 = (__double2hiint(v.y) & 0x7ff00000) == 0x7ff00000;
+    if (b0 || b1) {
+      const unsigned long long idx = (unsigned long long)(2 * i + (b0 ? 0 : 1));
+      best = idx < best ? idx : best;
+    }
+  }
+  if ((count & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const double v = x[count - 1];
+    if ((__double2hiint(v) & 0x7ff00000) == 0x7ff00000) best = best < (unsigned long long)(count - 1) ? best : count - 1;
+  }
+  if (__any_sync(0xffffffffu, best != ~0ull)) {
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
+      best = other < best ? other : best;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMin(first, best);
+  }
+}
+
+int first_nonfinite_run(const double* x, int64_t count, int64_t* first, cudaStream_t st) {
+  static_assert(sizeof(unsigned long long) == sizeof(int64_t), "index width");
+  TSNMF_CUDA_CHECK(cudaMemsetAsync(first, 0xff, sizeof(int64_t), st));  // -1: all finite
+  if (count <= 0) return kOk;
+  int sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = kNumSMs;
+  const int64_t want = ceil_div(max64(count >> 1, 1), 256);
+  const unsigned blocks = (unsigned)min64(want, (int64_t)sms * 8);
+  first_nonfinite_kernel<<<blocks, 256, 0, st>>>(x, count, reinterpret_cast<unsigned long long*>(first));
+  TSNMF_LAUNCH_CHECK();
+  return kOk;
+}
+
 }  // namespace tsnmf

@@ -196,6 +196,19 @@ def column_stats(x):
     return l1, sq
 
 
+def first_nonfinite(x) -> int:
+    """Linear (row-major) index of the first Inf/NaN of a contiguous device array, -1 if none
+    (reference matio.py:81-87 _check_finite, on the device)."""
+    t = torch()
+    if not (isinstance(x, t.Tensor) and x.is_cuda and x.dtype == t.float64 and x.is_contiguous()):
+        raise UsageError("first_nonfinite needs a contiguous CUDA float64 tensor")
+    dev = x.device
+    out = t.empty(1, dtype=t.int64, device=dev)
+    _native.call("tsnmf_first_nonfinite", x.data_ptr(), int(x.numel()), out.data_ptr(), stream_ptr(dev),
+                 stage="read")
+    return int(out.item())
+
+
 # ---------------------------------------------------------------------------
 # selection / coefficients (SURVEY §8f row 1)
 

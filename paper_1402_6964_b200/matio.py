@@ -1,9 +1,11 @@
 """Dense matrix files in the reference's binary layout (16-byte little-endian
 header: magic b"TS", version u16 = 1, rows u64, cols u32; then row-major
-float64; reference pkg/src/tsnmf/matio.py:1-25), used by the save/load
-sidecars of the result types, plus a row-chunk iterator over such files.
-The full reader/writer stack (text format, hashing, finiteness reports) is the
-SURVEY §8f "ingest" row and is not part of this round.
+float64; reference pkg/src/tsnmf/matio.py:1-25): read_matrix / write_matrix for
+the result types' sidecars, and ChunkReader — the reference's streaming reader
+(matio.py:90-156: same parameters, counters, content hashing and errors) with a
+device mode that feeds the B200 pass: large sequential reads
+into pinned buffers, copies on a side stream, the finiteness check on the device.
+The text format is not mirrored.
 """
 
 from __future__ import annotations
@@ -13,7 +15,7 @@ from pathlib import Path
 
 import numpy as np
 
-from .errors import DataError
+from .errors import DataError, UsageError
 from .rowchunk import RowChunk
 
 _HDR = struct.Struct("<2sHQI")
@@ -58,3 +60,177 @@ def iter_chunks(path, chunk_rows: int = 8192):
     mm = np.memmap(path, dtype="<f8", mode="r", offset=HEADER_BYTES, shape=(rows, cols))
     for off in range(0, rows, chunk_rows):
         yield RowChunk(row_offset=off, data=np.asarray(mm[off:off + chunk_rows]))
+
+
+DEFAULT_CHUNK_ROWS = 8192  # reference matio.py:27
+
+
+def _unpack_header_ref(raw: bytes) -> tuple[int, int]:
+    """Header checks with the reference's messages (matio.py:54-62, MatrixHeader :40-46)."""
+    if len(raw) < HEADER_BYTES:
+        raise DataError("malformed header: file shorter than header")
+    magic, version, rows, cols = _HDR.unpack(raw[:HEADER_BYTES])
+    if magic != b"TS":
+        raise DataError("malformed header: bad magic")
+    if version != 1:
+        raise DataError(f"malformed header: unsupported version {version}")
+    if cols < 1:
+        raise DataError(f"matrix must have at least one column, got {cols}")
+    return rows, cols
+
+
+def _nonfinite_error(block_row0: int, row_in_block: int, col: int) -> DataError:
+    # reference matio.py:81-87
+    return DataError(f"non-finite entry at row {block_row0 + row_in_block}, column {col}")
+
+
+class ChunkReader:
+    """Streams RowChunks from a binary matrix file (reference matio.py:90-156).
+
+    Parameters and attributes follow the reference: ``chunk_rows`` (rows per chunk, the last may be
+    shorter), ``validate`` (reject NaN/Inf, reporting the first bad row and column), ``hasher``
+    (hashlib-style object updated with every byte read, header included), ``rows_read`` /
+    ``bytes_read`` counters, and the same DataError / UsageError messages.
+
+    ``device`` (new): a CUDA device (``"cuda"``, ``torch.device`` or index) makes the reader yield
+    device-resident chunks.  Whole chunks are read in batches of ~``batch_bytes`` into one of two
+    pinned host buffers, copied to the device on a side stream (overlapping the consumer's kernels on
+    the current stream), validated on the device (``tsnmf_first_nonfinite``: one HBM sweep per batch),
+    and yielded as row views of the batch, so ``stream_pass`` reduces consecutive chunks as one batch.
+    Chunk boundaries, order, counters, hash and error positions are those of the host reader: chunks
+    before a non-finite entry are yielded, the error is raised when its chunk is reached.
+    """
+
+    def __init__(self, path, chunk_rows: int = DEFAULT_CHUNK_ROWS, *, validate: bool = True, hasher=None,
+                 device=None, batch_bytes: int = 1 << 30):
+        if chunk_rows < 1:
+            raise UsageError(f"chunk_rows must be >= 1, got {chunk_rows}")
+        self.path = Path(path)
+        self.chunk_rows = chunk_rows
+        self.validate = validate
+        self.hasher = hasher
+        self.device = device
+        self.batch_bytes = int(batch_bytes)
+        self.rows_read = 0
+        self.bytes_read = 0
+        size = self.path.stat().st_size
+        with open(self.path, "rb") as f:
+            raw = f.read(HEADER_BYTES)
+        self._rows, self._cols = _unpack_header_ref(raw)
+        expected = HEADER_BYTES + self._rows * self._cols * 8
+        if size < expected:
+            raise DataError("payload shorter than declared")
+        if size > expected:
+            raise DataError("payload longer than declared")
+
+    @property
+    def rows(self) -> int:
+        return self._rows
+
+    @property
+    def cols(self) -> int:
+        return self._cols
+
+    def __iter__(self):
+        if self.device is None:
+            return self._iter_host()
+        return self._iter_device()
+
+    def _read_header(self, f) -> None:
+        raw = f.read(HEADER_BYTES)
+        if self.hasher is not None:
+            self.hasher.update(raw)
+        self.bytes_read += len(raw)
+
+    def _iter_host(self):
+        n = self._cols
+        with open(self.path, "rb") as f:
+            self._read_header(f)
+            offset = 0
+            while offset < self._rows:
+                c = min(self.chunk_rows, self._rows - offset)
+                raw = f.read(c * n * 8)
+                if len(raw) < c * n * 8:
+                    raise DataError("payload shorter than declared")
+                if self.hasher is not None:
+                    self.hasher.update(raw)
+                self.bytes_read += len(raw)
+                block = np.frombuffer(raw, dtype="<f8").reshape(c, n)
+                if self.validate and not np.isfinite(block).all():
+                    bad = np.argwhere(~np.isfinite(block))[0]
+                    raise _nonfinite_error(offset, int(bad[0]), int(bad[1]))
+                self.rows_read += c
+                yield RowChunk(row_offset=offset, data=block)
+                offset += c
+
+    def _iter_device(self):
+        from . import device as dv
+
+        t = dv.torch()
+        dev = t.device(self.device) if not isinstance(self.device, int) else t.device("cuda", self.device)
+        if dev.type != "cuda":
+            raise UsageError(f"ChunkReader device must be a CUDA device, got {self.device!r}")
+        if dev.index is None:
+            dev = t.device("cuda", t.cuda.current_device())
+        n = self._cols
+        row_bytes = n * 8
+        per_batch = max(1, self.batch_bytes // (row_bytes * self.chunk_rows)) * self.chunk_rows
+        per_batch = min(per_batch, max(self._rows, 1))
+        host = [t.empty((per_batch, n), dtype=t.float64).pin_memory() for _ in range(2)]
+        views = [memoryview(h.numpy()).cast("B") for h in host]
+        copy_stream = t.cuda.Stream(dev)
+        compute = t.cuda.current_stream(dev)
+        batches = [(o, min(per_batch, self._rows - o)) for o in range(0, self._rows, per_batch)]
+        from concurrent.futures import ThreadPoolExecutor
+
+        with open(self.path, "rb") as f, ThreadPoolExecutor(max_workers=1) as pool:
+            self._read_header(f)
+
+            def read_into(k, rows):  # worker thread: sequential reads (the GIL is released while reading)
+                return f.readinto(views[k][:rows * row_bytes])
+
+            # read-ahead: batch i+1 is read into the other pinned buffer while batch i is copied, scanned and
+            # consumed; that buffer's previous copy finished at the scan's synchronisation point
+            pending = pool.submit(read_into, 0, batches[0][1]) if batches else None
+            for i, (offset, rows) in enumerate(batches):
+                k = i & 1
+                got = pending.result()
+                view = views[k]
+                if got < rows * row_bytes:
+                    # the reference reads chunk by chunk: account for the whole chunks it would deliver
+                    self._account(view, got // (self.chunk_rows * row_bytes) * self.chunk_rows, offset, n)
+                    raise DataError("payload shorter than declared")
+                hb = host[k][:rows]
+                with t.cuda.stream(copy_stream):  # copy + device scan: only this stream is waited on
+                    xb = t.empty((rows, n), dtype=t.float64, device=dev)
+                    xb.copy_(hb, non_blocking=True)
+                    ev = t.cuda.Event()
+                    ev.record(copy_stream)
+                    bad = dv.first_nonfinite(xb) if self.validate else -1
+                    if not self.validate:
+                        ev.synchronize()  # host buffer k is refilled next: its copy must be done
+                compute.wait_event(ev)
+                xb.record_stream(compute)
+                if i + 1 < len(batches):
+                    pending = pool.submit(read_into, k ^ 1, batches[i + 1][1])
+                good_rows = rows if bad < 0 else (bad // n)
+                for r0 in range(0, rows, self.chunk_rows):
+                    c = min(self.chunk_rows, rows - r0)
+                    raw = view[r0 * row_bytes:(r0 + c) * row_bytes]
+                    if self.hasher is not None:
+                        self.hasher.update(raw)
+                    self.bytes_read += len(raw)
+                    if bad >= 0 and r0 + c > good_rows:
+                        raise _nonfinite_error(offset + r0, good_rows - r0, int(bad % n))
+                    self.rows_read += c
+                    yield RowChunk(row_offset=offset + r0, data=xb[r0:r0 + c])
+
+    def _account(self, view, whole_rows: int, offset: int, n: int) -> None:
+        """Counters and hash for the whole chunks read before a short payload (reference behaviour)."""
+        row_bytes = n * 8
+        for r0 in range(0, whole_rows, self.chunk_rows):
+            raw = view[r0 * row_bytes:(r0 + self.chunk_rows) * row_bytes]
+            if self.hasher is not None:
+                self.hasher.update(raw)
+            self.bytes_read += len(raw)
+            self.rows_read += self.chunk_rows
