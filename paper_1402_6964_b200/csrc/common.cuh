@@ -202,11 +202,24 @@ __device__ __forceinline__ double bm_cos(double t, uint64_t w2) {
 // z = sqrt(-2 log u1) cos(2 pi u2) with the same rounding of u1, u2 and 2 pi u2 as the reference; log
 // and cos are the domain-specialised bm_log / bm_cos (few-ulp, ~100 instructions per normal instead of
 // ~250 with the general libdevice versions).  Agreement with the reference's libm: |dz| <= ~1e-15.
+// sqrt(x) for x in [1e-16, 80] (the Box-Muller radius argument -2 log u1): MUFU approximation of 1/sqrt,
+// two Newton steps, then one residual correction of s = x y — within 1 ulp of the correctly rounded root,
+// and branch-free (the IEEE sqrt's special-value path is a call), so the generator stays one basic block.
+__device__ __forceinline__ double bm_sqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  const double s = x * y;
+  return fma(0.5 * y, fma(-s, s, x), s);
+}
+
 __device__ __forceinline__ double rng_normal(uint64_t stream, uint64_t j) {
   double u1 = __dmul_rn(__dadd_rn((double)(rng_word(stream, 2 * j) >> 11), 0.5), kInv2p53);
   const uint64_t w2 = rng_word(stream, 2 * j + 1) >> 11;
   double u2 = __dmul_rn((double)w2, kInv2p53);
-  return __dmul_rn(sqrt(__dmul_rn(-2.0, bm_log(u1))), bm_cos(__dmul_rn(kTwoPi, u2), w2));
+  return __dmul_rn(bm_sqrt(__dmul_rn(-2.0, bm_log(u1))), bm_cos(__dmul_rn(kTwoPi, u2), w2));
 }
 
 // Single-precision Box-Muller on the same counters (2j, 2j+1), used ONLY by the synthetic-data
