@@ -1,3 +1,4 @@
+"""GX: fused in-CTA generation vs the two-kernel path (TSNMF_SK_FUSED=0) — agreement and timing."""
 import sys, os
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch

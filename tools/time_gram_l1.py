@@ -1,3 +1,4 @@
+"""Gram with and without the fused column l1 (its cost per width)."""
 import sys, os
 sys.path.insert(0, os.getcwd())
 import torch
