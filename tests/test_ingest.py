@@ -110,3 +110,18 @@ def test_device_reader_nonfinite_like_host(tmp_path, bad_row, bad_col):
         outs.append((str(e.value), seen, r.rows_read, r.bytes_read))
     assert outs[0] == outs[1]
     assert f"row {bad_row}, column {bad_col}" in outs[0][0]
+
+
+@pytest.mark.gpu
+def test_device_reader_edge_cases(tmp_path):
+    """Empty payload (the pass reports the reference's empty-stream error), validation off (NaN passes
+    through to the factor as in the reference), a single short batch."""
+    p0 = _file(tmp_path, np.zeros((0, 5)), "empty.bin")
+    assert _drain(ChunkReader(p0, device="cuda")) == []
+    with pytest.raises(DataError, match="empty chunk stream"):
+        tb.stream_pass(ChunkReader(p0, device="cuda"))
+    x = np.random.default_rng(3).uniform(0, 1, (777, 9))
+    x[5, 5] = np.nan
+    p1 = _file(tmp_path, x, "nan.bin")
+    got = _drain(ChunkReader(p1, chunk_rows=100, device="cuda", validate=False))
+    assert np.isnan(np.vstack([d for _, d in got])[5, 5]) and len(got) == 8
