@@ -73,9 +73,10 @@ __device__ __forceinline__ double rng_uniform(uint64_t stream, uint64_t ctr) {
   return __dmul_rn((double)(rng_word(stream, ctr) >> 11), kInv2p53);
 }
 
+
 // Box-Muller polynomial coefficients in the constant bank: DFMA reads them as c[] operands instead of
 // materialising each 64-bit immediate with two uniform moves per use (~60 UMOVs per normal).
-static __constant__ double kBmC[31] = {
+static __constant__ double kBmLogPolyC[31] = {
     0.05263157894736842,
     0.058823529411764705,
     0.06666666666666667,
@@ -107,11 +108,10 @@ static __constant__ double kBmC[31] = {
     -0.16666666666666666,
     1.0,
     -8.22063524662433e-18};
-
-// log(u) for u in [2^-54, 1) (the Box-Muller u1 domain): u = m 2^e with m in [sqrt(1/2), sqrt(2)),
+// log(u), polynomial form, for u in [2^-54, 1) (the Box-Muller u1 domain): u = m 2^e with m in [sqrt(1/2), sqrt(2)),
 // log m = 2 atanh(s), s = (m - 1)/(m + 1), |s| <= 0.1716, atanh series through s^21; ln 2 split hi/lo.
 // No special-value paths are needed on this domain.  Max relative error ~4e-16 vs libm (1M samples).
-__device__ __forceinline__ double bm_log(double u) {
+__device__ __forceinline__ double bm_log_poly(double u) {
   const int hi = __double2hiint(u), lo = __double2loint(u);
   int e = ((hi >> 20) & 0x7ff) - 1023;
   double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);  // [1, 2)
@@ -127,19 +127,99 @@ __device__ __forceinline__ double bm_log(double u) {
   double sv = f * r;
   sv = fma(r, fma(-sv, den, f), sv);  // one residual correction: s to ~0.5 ulp
   const double z = sv * sv;
-  double p = kBmC[10];
-  p = fma(p, z, kBmC[0]);
-  p = fma(p, z, kBmC[1]);
-  p = fma(p, z, kBmC[2]);
-  p = fma(p, z, kBmC[3]);
-  p = fma(p, z, kBmC[4]);
-  p = fma(p, z, kBmC[5]);
-  p = fma(p, z, kBmC[6]);
-  p = fma(p, z, kBmC[7]);
-  p = fma(p, z, kBmC[8]);
-  p = fma(p, z, kBmC[9]);
+  double p = kBmLogPolyC[10];
+  p = fma(p, z, kBmLogPolyC[0]);
+  p = fma(p, z, kBmLogPolyC[1]);
+  p = fma(p, z, kBmLogPolyC[2]);
+  p = fma(p, z, kBmLogPolyC[3]);
+  p = fma(p, z, kBmLogPolyC[4]);
+  p = fma(p, z, kBmLogPolyC[5]);
+  p = fma(p, z, kBmLogPolyC[6]);
+  p = fma(p, z, kBmLogPolyC[7]);
+  p = fma(p, z, kBmLogPolyC[8]);
+  p = fma(p, z, kBmLogPolyC[9]);
   const double de = (double)e;
   return fma(de, 0.6931471803691238, fma(de, 1.9082149292705877e-10, 2.0 * sv * p));
+}
+
+// log(u) for u in [2^-54, 1) (the Box-Muller u1 domain): table-driven.  u = 2^e m, m in [1, 2); for
+// m >= 1.5 use m/2 and e+1, so m' in [0.75, 1.5) (u near 1 keeps e' = 0: no cancellation); j = round(64 m')
+// from the mantissa bits, f = m' inv_j - 1 (|f| <= 0.0105, one rounding), log1p(f) through f^9 (truncation
+// < 2e-21), log u = e' ln2 + L_j + log1p(f) with L_j = -ln(inv_j) (hi + lo, the exact logarithm of the
+// stored reciprocal).  ~14 FP64 operations instead of ~21; ~1 ulp.  Table: tools/gen_bm_tables.py log.
+// LN2_HI = 0x1.62e42fefa3a00p-1, LN2_LO = -0x1.0ca86c3898d00p-49
+static __device__ const double4 kBmLogTab[49] = {
+    {0x1.5555555555555p+0, -0x1.269621134db91p-2, -0x1.e0efadd9db02ap-56, 0.0},  // j = 48
+    {0x1.4e5e0a72f0539p+0, -0x1.1178e8227e47ap-2, -0x1.b8ce2d07f1cb7p-56, 0.0},  // j = 49
+    {0x1.47ae147ae147bp+0, -0x1.f991c6cb3b37ap-3, -0x1.ecca0cdf30143p-58, 0.0},  // j = 50
+    {0x1.4141414141414p+0, -0x1.d1037f2655e7bp-3, 0x1.3f3adb7b71cbcp-58, 0.0},  // j = 51
+    {0x1.3b13b13b13b14p+0, -0x1.a93ed3c8ad9e5p-3, -0x1.bcafa9de97202p-57, 0.0},  // j = 52
+    {0x1.3521cfb2b78c1p+0, -0x1.823c16551a3c0p-3, -0x1.6dcd318f4187ep-57, 0.0},  // j = 53
+    {0x1.2f684bda12f68p+0, -0x1.5bf406b543db0p-3, 0x1.1f5b44c0df7f7p-61, 0.0},  // j = 54
+    {0x1.29e4129e4129ep+0, -0x1.365fcb0159014p-3, -0x1.bea08d2dca256p-57, 0.0},  // j = 55
+    {0x1.2492492492492p+0, -0x1.1178e8227e47ap-3, 0x1.0e63a5f01c693p-58, 0.0},  // j = 56
+    {0x1.1f7047dc11f70p+0, -0x1.da7276384469ep-4, -0x1.401fa71733017p-58, 0.0},  // j = 57
+    {0x1.1a7b9611a7b96p+0, -0x1.9335e5d594988p-4, 0x1.478a85704ccb7p-58, 0.0},  // j = 58
+    {0x1.15b1e5f75270dp+0, -0x1.4d3115d207eacp-4, -0x1.da7d0b1e10b2fp-60, 0.0},  // j = 59
+    {0x1.1111111111111p+0, -0x1.08598b59e3a06p-4, 0x1.dd7009902bf32p-58, 0.0},  // j = 60
+    {0x1.0c9714fbcda3bp+0, -0x1.894aa149fb34bp-5, 0x1.2ba0b44cfaee5p-59, 0.0},  // j = 61
+    {0x1.0842108421084p+0, -0x1.0415d89e74440p-5, -0x1.c05cf1d753621p-59, 0.0},  // j = 62
+    {0x1.0410410410410p+0, -0x1.0205658935837p-6, -0x1.27c8e8416e717p-60, 0.0},  // j = 63
+    {0x1.0000000000000p+0, 0x0.0p+0, 0x0.0p+0, 0.0},  // j = 64
+    {0x1.f81f81f81f820p-1, 0x1.fc0a8b0fc03c4p-7, -0x1.83092c5964281p-62, 0.0},  // j = 65
+    {0x1.f07c1f07c1f08p-1, 0x1.f829b0e7832f8p-6, 0x1.33e3f04f1ef25p-60, 0.0},  // j = 66
+    {0x1.e9131abf0b767p-1, 0x1.77458f632dcffp-5, 0x1.8d3ca87b92968p-63, 0.0},  // j = 67
+    {0x1.e1e1e1e1e1e1ep-1, 0x1.f0a30c01162a8p-5, 0x1.85f325c5bbacdp-59, 0.0},  // j = 68
+    {0x1.dae6076b981dbp-1, 0x1.341d7961bd1d0p-4, -0x1.3599f227becbbp-58, 0.0},  // j = 69
+    {0x1.d41d41d41d41dp-1, 0x1.6f0d28ae56b4ep-4, -0x1.20db323097324p-59, 0.0},  // j = 70
+    {0x1.cd85689039b0bp-1, 0x1.a926d3a4ad562p-4, -0x1.d7a16eab1e2adp-59, 0.0},  // j = 71
+    {0x1.c71c71c71c71cp-1, 0x1.e27076e2af2eap-4, -0x1.61578001e015ap-60, 0.0},  // j = 72
+    {0x1.c0e070381c0e0p-1, 0x1.0d77e7cd08e5bp-3, 0x1.9a5dc5e9030adp-57, 0.0},  // j = 73
+    {0x1.bacf914c1bad0p-1, 0x1.29552f81ff521p-3, 0x1.301771c407dc0p-57, 0.0},  // j = 74
+    {0x1.b4e81b4e81b4fp-1, 0x1.44d2b6ccb7d1cp-3, 0x1.7d3d950f87e23p-59, 0.0},  // j = 75
+    {0x1.af286bca1af28p-1, 0x1.5ff3070a793d6p-3, -0x1.bc60efafc6f6cp-58, 0.0},  // j = 76
+    {0x1.a98ef606a63bep-1, 0x1.7ab890210d907p-3, -0x1.1072534a57e7dp-57, 0.0},  // j = 77
+    {0x1.a41a41a41a41ap-1, 0x1.9525a9cf456b6p-3, -0x1.26fb3e2b1d1dap-57, 0.0},  // j = 78
+    {0x1.9ec8e951033d9p-1, 0x1.af3c94e80bff3p-3, 0x1.a3398064df33ep-57, 0.0},  // j = 79
+    {0x1.999999999999ap-1, 0x1.c8ff7c79a9a20p-3, -0x1.4f689f8434011p-57, 0.0},  // j = 80
+    {0x1.948b0fcd6e9e0p-1, 0x1.e27076e2af2e8p-3, -0x1.61578001e015ep-59, 0.0},  // j = 81
+    {0x1.8f9c18f9c18fap-1, 0x1.fb9186d5e3e29p-3, 0x1.355519b0de535p-57, 0.0},  // j = 82
+    {0x1.8acb90f6bf3aap-1, 0x1.0a324e27390e2p-2, 0x1.bdcfde8061c03p-56, 0.0},  // j = 83
+    {0x1.8618618618618p-1, 0x1.1675cababa60fp-2, 0x1.ce63eab883727p-61, 0.0},  // j = 84
+    {0x1.8181818181818p-1, 0x1.22941fbcf7966p-2, -0x1.dbd7ac258a2bdp-58, 0.0},  // j = 85
+    {0x1.7d05f417d05f4p-1, 0x1.2e8e2bae11d31p-2, -0x1.1e99b72bd7bf2p-57, 0.0},  // j = 86
+    {0x1.78a4c8178a4c8p-1, 0x1.3a64c556945eap-2, 0x1.cbcd735d03424p-60, 0.0},  // j = 87
+    {0x1.745d1745d1746p-1, 0x1.4618bc21c5ec2p-2, -0x1.7a42642661c62p-61, 0.0},  // j = 88
+    {0x1.702e05c0b8170p-1, 0x1.51aad872df82ep-2, -0x1.d8db0a7cc1543p-56, 0.0},  // j = 89
+    {0x1.6c16c16c16c17p-1, 0x1.5d1bdbf5809cap-2, -0x1.7dc9c7c23801fp-56, 0.0},  // j = 90
+    {0x1.6816816816817p-1, 0x1.686c81e9b14adp-2, 0x1.710af840538e3p-56, 0.0},  // j = 91
+    {0x1.642c8590b2164p-1, 0x1.739d7f6bbd007p-2, 0x1.ce24c53fad3f0p-58, 0.0},  // j = 92
+    {0x1.6058160581606p-1, 0x1.7eaf83b82afc2p-2, -0x1.698b43096b576p-59, 0.0},  // j = 93
+    {0x1.5c9882b931057p-1, 0x1.89a3386c1425bp-2, 0x1.2d38c40881e0bp-57, 0.0},  // j = 94
+    {0x1.58ed2308158edp-1, 0x1.947941c2116fbp-2, 0x1.1266e8a3e8838p-57, 0.0},  // j = 95
+    {0x1.5555555555555p-1, 0x1.9f323ecbf984dp-2, -0x1.a92e513217f58p-59, 0.0},  // j = 96
+};
+static __constant__ double kBmLogC[8] = {1.0 / 9, -1.0 / 8, 1.0 / 7, -1.0 / 6, 1.0 / 5, -1.0 / 4, 1.0 / 3, -0.5};
+__device__ __forceinline__ double bm_log_tab(double u) {
+  const int hi = __double2hiint(u), lo = __double2loint(u);
+  const int ftop = hi & 0x000fffff;  // top 20 bits of the mantissa field
+  const bool big = ftop >= 0x80000;  // m >= 1.5
+  const int e = ((hi >> 20) & 0x7ff) - 1023 + (big ? 1 : 0);
+  const int j = big ? 32 + ((ftop + 0x4000) >> 15) : 64 + ((ftop + 0x2000) >> 14);  // round(64 m'), 48..96
+  const double mp = __hiloint2double(ftop | (big ? 0x3fe00000 : 0x3ff00000), lo);
+  const double2 t0 = __ldg(reinterpret_cast<const double2*>(&kBmLogTab[j - 48]));
+  const double2 t1 = __ldg(reinterpret_cast<const double2*>(&kBmLogTab[j - 48]) + 1);
+  const double f = fma(mp, t0.x, -1.0);
+  double q = fma(f, kBmLogC[0], kBmLogC[1]);
+  q = fma(q, f, kBmLogC[2]);
+  q = fma(q, f, kBmLogC[3]);
+  q = fma(q, f, kBmLogC[4]);
+  q = fma(q, f, kBmLogC[5]);
+  q = fma(q, f, kBmLogC[6]);
+  q = fma(q, f, kBmLogC[7]);
+  const double lp = fma(f * f, q, f);
+  const double de = (double)e;
+  return fma(de, 0x1.62e42fefa3a00p-1, t0.y) + (fma(de, -0x1.0ca86c3898d00p-49, t1.x) + lp);
 }
 
 // cos(t) for t = fl(2 pi u2), u2 = w2 2^-53 (the Box-Muller angle): table-driven.  k = round(64 u2) from
@@ -215,11 +295,16 @@ __device__ __forceinline__ double bm_sqrt(double x) {
   return fma(0.5 * y, fma(-s, s, x), s);
 }
 
+// kTabLog selects the log form: the table one (fewer FP64 operations, two extra L1 loads) is faster for the
+// standalone generator and the narrow sketch slabs; inside the n = 200 contraction the polynomial one is
+// (its slabs already keep the shared-memory / L1 path busy).  Both within ~1 ulp of libm.
+template <bool kTabLog = true>
 __device__ __forceinline__ double rng_normal(uint64_t stream, uint64_t j) {
   double u1 = __dmul_rn(__dadd_rn((double)(rng_word(stream, 2 * j) >> 11), 0.5), kInv2p53);
   const uint64_t w2 = rng_word(stream, 2 * j + 1) >> 11;
   double u2 = __dmul_rn((double)w2, kInv2p53);
-  return __dmul_rn(bm_sqrt(__dmul_rn(-2.0, bm_log(u1))), bm_cos(__dmul_rn(kTwoPi, u2), w2));
+  const double lg = kTabLog ? bm_log_tab(u1) : bm_log_poly(u1);
+  return __dmul_rn(bm_sqrt(__dmul_rn(-2.0, lg)), bm_cos(__dmul_rn(kTwoPi, u2), w2));
 }
 
 // Single-precision Box-Muller on the same counters (2j, 2j+1), used ONLY by the synthetic-data

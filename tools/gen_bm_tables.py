@@ -49,5 +49,30 @@ for k in range(33):
     s, c = sincos(P * k)
     s, c = (Decimal(0) if abs(s) < Decimal(10) ** -40 else s), (Decimal(0) if abs(c) < Decimal(10) ** -40 else c)
     rows.append(f"    {{{hexd(float(c))}, {hexd(float(s))}}},  // k = {k}")
-print(f"// C1 = {hexd(c1)}, C2 = {hexd(c2)}")
-print("\n".join(rows))
+if len(__import__("sys").argv) == 1:
+    print(f"// C1 = {hexd(c1)}, C2 = {hexd(c2)}")
+    print("\n".join(rows))
+
+
+def log_table():
+    """Box-Muller log table (common.cuh kBmLogTab): for j = 48..96, inv_j = 64/j rounded to double and
+    -ln(inv_j) (the exact logarithm of the stored reciprocal) as a hi + lo pair; ln 2 as hi (44 bits) +
+    lo."""
+    rows = []
+    for j in range(48, 97):
+        inv = float(Decimal(64) / Decimal(j))
+        L = -Decimal(inv).ln()
+        hi = float(L)
+        lo = float(L - Decimal(hi))
+        rows.append(f"    {{{hexd(inv)}, {hexd(hi)}, {hexd(lo)}, 0.0}},  // j = {j}")
+    ln2 = Decimal(2).ln()
+    m, e = __import__("math").frexp(float(ln2))
+    l2hi = __import__("math").ldexp(round(m * 2 ** 44) / 2 ** 44, e)
+    l2lo = float(ln2 - Decimal(l2hi))
+    return f"// LN2_HI = {hexd(l2hi)}, LN2_LO = {hexd(l2lo)}", rows
+
+
+if __name__ == "__main__" and len(__import__("sys").argv) > 1 and __import__("sys").argv[1] == "log":
+    h, r = log_table()
+    print(h)
+    print("\n".join(r))
