@@ -909,6 +909,10 @@ struct WlGeom {
 #endif
 constexpr int wl_sync(int n) { return n >= 24 ? TSNMF_WL_SYNC : 0; }
 
+// Packed upper-triangular R of the narrow leaf: row i starts at wl_roff(N, i) + i (R(i, c) at wl_roff + c):
+// n(n+1)/2 doubles instead of n^2 (n = 25: one more warp per SM fits).
+__host__ __device__ constexpr int wl_roff(int n, int i) { return i * n - i * (i - 1) / 2 - i; }
+
 template <int N, int S>
 __global__ void __launch_bounds__(256)
     tsqr_warp_leaf_kernel(const double* __restrict__ x, int64_t m, int64_t ldx, int64_t rows_per_warp, int nleaves,
@@ -921,14 +925,14 @@ __global__ void __launch_bounds__(256)
   uint64_t* bar = reinterpret_cast<uint64_t*>(base);
   double* stg = base + g.stage_off;
   double* P = base + g.prod_off;
-  double* Rs = base + g.r_off;  // R(i, c) at Rs[i * N + c]
+  double* Rs = base + g.r_off;  // R(i, c), c >= i, packed by rows at Rs[wl_roff(N, i) + c]
   double* TW = base + g.tw_off;
   const int64_t leaf = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;  // surplus warps (leaf >= nleaves) idle
   const int64_t rbeg = leaf * rows_per_warp;
   const int64_t rend = min64(m, rbeg + rows_per_warp);
   const int64_t nblk = rows_per_warp / BR;
   constexpr int kWlSync = wl_sync(N);
-  for (int i = lane; i < N * N; i += 32) Rs[i] = 0.0;
+  for (int i = lane; i < N * (N + 1) / 2; i += 32) Rs[i] = 0.0;
   for (int i = lane; i < N + 1; i += 32) TW[i] = 0.0;
   if (lane == 0) {
     mbar_init(bar, 1);
@@ -1023,8 +1027,8 @@ __global__ void __launch_bounds__(256)
       const int col = j + 1 + (lane & (L - 1));
       const int grow = (lane & ~(L - 1)) & 31;
       // R row j is only changed by reflector j, so R(j, .) is read up front (off the chain)
-      const double rjc = Rs[j * N + (col < N ? col : N - 1)];
-      const double alpha = Rs[j * N + j];
+      const double rjc = Rs[wl_roff(N, j) + (col < N ? col : N - 1)];
+      const double alpha = Rs[wl_roff(N, j) + j];
       double d = 0.0;
 #pragma unroll
       for (int q = 0; q < S; ++q) d = fma(xr[q][j], xr[q][j], d);
@@ -1094,11 +1098,11 @@ __global__ void __launch_bounds__(256)
         for (int o = L; o < 32; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
         const double tw = tau * (rjc + sum);
         if (lane < L && col < N) {
-          Rs[j * N + col] = rjc - tw;
+          Rs[wl_roff(N, j) + col] = rjc - tw;
           TW[col] = tw;
         }
       }
-      if (lane == j) Rs[j * N + j] = beta;
+      if (lane == j) Rs[wl_roff(N, j) + j] = beta;
       if (j + 1 < N) {
         __syncwarp();
         // critical: the next pivot column now; the rest is deferred into step j+1
@@ -1118,7 +1122,7 @@ __global__ void __launch_bounds__(256)
   double* R = slots + leaf * g.npad * g.npad;
   if (lane < g.npad) {
     for (int i = 0; i < g.npad; ++i)
-      R[(int64_t)i * g.npad + lane] = (i < N && lane < N && i <= lane) ? Rs[i * N + lane] : 0.0;
+      R[(int64_t)i * g.npad + lane] = (i < N && lane < N && i <= lane) ? Rs[wl_roff(N, i) + lane] : 0.0;
     if (stats) {
       double a = 0.0, q = 0.0;
       if (lane < N)
@@ -1320,7 +1324,7 @@ WlGeom warp_leaf_geom(int n, int S) {
   g.stage_off = 2;  // [0, 2): mbarrier
   g.prod_off = g.stage_off + (int)round_up(32 * S * g.ls, 2);
   g.r_off = g.prod_off + (int)round_up(32 * g.pld, 2);
-  g.tw_off = g.r_off + (int)round_up(n * n, 2);
+  g.tw_off = g.r_off + (int)round_up(n * (n + 1) / 2, 2);  // R packed upper triangle
   g.total = g.tw_off + (int)round_up(n + 1, 2);
   return g;
 }
