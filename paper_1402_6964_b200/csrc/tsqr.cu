@@ -14,9 +14,12 @@
 // per column); the next panel's columns get the lookahead update from the panel warp + helper pair and
 // the rest of the trailing matrix the compact-WY update  W = R_p + V^T B,  W <- T^T W,  R_p -= W,
 // B -= V W  by six GEMM warps on FP64 tensor cores (mma.sync m8n8k4 f64 = DMMA), overlapped with the
-// next panel.  Narrow matrices (n <= 32) use a warp-per-chain leaf instead (tsqr_small_leaf_kernel).  Leaves are then combined in the reference TreeReducer order (perfect
-// binary levels over the leaf index, then a fold of the leftover subtrees), each combine being the same
-// structured QR with the second factor's rows as data (triangular: panels left of the block are skipped).
+// next panel.  Narrow matrices (n <= 32) use the register-block warp leaf instead (tsqr_warp_leaf_kernel:
+// one Householder chain per warp over 32*S-row blocks held in registers; the older 32-row
+// tsqr_small_leaf_kernel stays selectable and is the narrow combine).  Leaves are then combined in the
+// reference TreeReducer order (perfect binary levels over the leaf index, then a fold of the leftover
+// subtrees), each combine being the same structured QR with the second factor's rows as data
+// (triangular: panels left of the block are skipped).
 #include <utility>
 
 #include "common.cuh"
