@@ -80,14 +80,13 @@ __global__ void __launch_bounds__(32 * WARPS, 1)
   for (int u = 0; u < SPW; ++u)
 #pragma unroll
     for (int t = 0; t < 4; ++t) acc[u][t][0] = acc[u][t][1] = 0.0;
-  constexpr int kL1H = (512 + (32 * WARPS) - 1) / (32 * WARPS);  // columns per thread for n <= 512
-  double l1a[kL1H];
-#pragma unroll
-  for (int h = 0; h < kL1H; ++h) l1a[h] = 0.0;
+  double l1x = 0.0, l1y = 0.0;  // this thread's column pair (l1_c, l1_c + 1)
   const bool do_l1 = (group == 0) && (l1part != nullptr);
-  // column l1: narrow matrices split each column's rows over l1_ph thread phases
-  const int l1_ph = g.npad <= (32 * WARPS) / 2 ? (32 * WARPS) / g.npad : 1;
-  const int l1_c = tid % g.npad, l1_r0 = tid / g.npad;
+  // column l1: each thread sums a column PAIR (16-byte loads; the swizzle keeps pairs adjacent) over the
+  // rows of its phase; the pairs' rows are split over l1_ph thread phases
+  const int npairs = g.npad / 2;
+  const int l1_ph = (32 * WARPS) / npairs;  // >= 1 for npad <= 1024
+  const int l1_c = 2 * (tid % npairs), l1_r0 = tid / npairs;
   const int frag_col = (lane >> 2) ^ ((lane & 2) << 1);  // swizzled slab fragment: row i + l%4, col l/4
 
   const int64_t nstages = ceil_div(max64(rend - rbeg, 0), br);
@@ -108,32 +107,15 @@ __global__ void __launch_bounds__(32 * WARPS, 1)
     __syncthreads();
     const double* xs = smem + (s & 1) * br * lds;
     if (do_l1) {
-      if (l1_ph > 1) {
-        // narrow: thread = (row phase, column); rows i = phase (mod l1_ph)
-        if (l1_r0 < l1_ph && l1_c < g.n) {
-          double a = 0.0;
-          for (int i = l1_r0; i < br; i += l1_ph) a += fabs(xs[i * lds + swz_col(i, l1_c)]);
-          l1a[0] += a;
+      if (l1_r0 < l1_ph && l1_c < g.n) {
+        double a0 = 0.0, a1 = 0.0;
+        for (int i = l1_r0; i < br; i += l1_ph) {
+          const double2 v = *reinterpret_cast<const double2*>(xs + i * lds + swz_col(i, l1_c));
+          a0 += fabs(v.x);
+          a1 += fabs(v.y);
         }
-      } else {
-#pragma unroll
-        for (int h = 0; h < kL1H; ++h) {
-          const int col = tid + h * (32 * WARPS);
-          if (col < g.n) {
-            // 4 independent chains so the adds pipeline (br % 4 == 0; rows 4j+2, 4j+3 are XOR-4 swizzled);
-            // the summation order is fixed, so the result stays deterministic
-            const double* p = xs + col;
-            const double* q = xs + (col ^ 4);
-            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-            for (int i = 0; i < br; i += 4) {
-              a0 += fabs(p[(i + 0) * lds]);
-              a1 += fabs(p[(i + 1) * lds]);
-              a2 += fabs(q[(i + 2) * lds]);
-              a3 += fabs(q[(i + 3) * lds]);
-            }
-            l1a[h] += (a0 + a1) + (a2 + a3);
-          }
-        }
+        l1x += a0;
+        l1y += a1;
       }
     }
     // branch-free DMMA issue: padding super-tiles (u >= nvalid) compute on (0, 0) and are not stored;
@@ -167,22 +149,17 @@ __global__ void __launch_bounds__(32 * WARPS, 1)
       dst[row * 16 + col + 1] = acc[u][t][1];
     }
   }
-  if (do_l1) {
-    if (l1_ph > 1) {  // fixed-order sum of the phases through shared memory
-      __syncthreads();
-      smem[tid] = (l1_r0 < l1_ph) ? l1a[0] : 0.0;
-      __syncthreads();
-      if (tid < g.npad) {
-        double a = 0.0;
-        for (int r = 0; r < l1_ph; ++r) a += smem[r * g.npad + tid];
-        l1part[split * g.npad + tid] = a;
-      }
-    } else {
-#pragma unroll
-      for (int h = 0; h < kL1H; ++h) {
-        const int col = tid + h * (32 * WARPS);
-        if (col < g.npad) l1part[split * g.npad + col] = l1a[h];
-      }
+  if (do_l1) {  // fixed-order sum of the row phases through shared memory
+    __syncthreads();
+    if (l1_r0 < l1_ph) {
+      smem[l1_r0 * g.npad + l1_c] = l1x;
+      smem[l1_r0 * g.npad + l1_c + 1] = l1y;
+    }
+    __syncthreads();
+    for (int c = tid; c < g.npad; c += 32 * WARPS) {
+      double a = 0.0;
+      for (int r = 0; r < l1_ph; ++r) a += smem[r * g.npad + c];
+      l1part[split * g.npad + c] = a;
     }
   }
 }
