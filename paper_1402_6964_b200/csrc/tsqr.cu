@@ -962,12 +962,13 @@ struct WlGeom {
 };
 
 
-// CTA barrier every wl_sync(N) column steps (0: none).  The warps of a CTA run the same straight-line
-// column code; for wide blocks (N >= 24: ~150 KB of code per block fold) keeping them within a few columns
-// of each other lets them share instruction-cache lines (measured n=25: 871 -> 906 GB/s with 4; narrower
-// code fits the cache and the barrier only costs: n=17 1244 -> 1169).
+// CTA barrier every wl_sync column steps (0: none; >= 32: once per row block, at its first column).  The
+// warps of a CTA run the same straight-line column code; keeping them in step lets them share
+// instruction-cache lines (the unrolled fold is ~100 KB of code at n = 25).  Measured at n = 25 (8 warps):
+// none 1023, every 2 columns 971, every 4 997, every 8 1021, every 12 1041, once per block 1063 GB/s;
+// narrower code fits the cache and the barrier only costs (n = 17: 1394 without, 1352 with).
 #ifndef TSNMF_WL_SYNC
-#define TSNMF_WL_SYNC 4
+#define TSNMF_WL_SYNC 32
 #endif
 constexpr int wl_sync(int n) { return n >= 24 ? TSNMF_WL_SYNC : 0; }
 
