@@ -589,17 +589,6 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
   if (init_zero) {
     for (int64_t idx = tid; idx < (int64_t)npad * npad; idx += kTqThreads) R[idx] = 0.0;
   }
-  // column stats: warps 1..7 (224 threads) sum column PAIRS (16-byte loads) over row phases; the panel
-  // warp takes none, so its first panel of every block starts right after staging
-  const int npairs = npad / 2;
-  const int st = tid - 32;
-  const int nph = npairs <= 224 ? 224 / npairs : 1;
-  const int st_pair = st >= 0 ? (npairs <= 224 ? st % npairs : st) : 0;
-  const int st_ph = st >= 0 ? (npairs <= 224 ? st / npairs : 0) : nph;  // nph: inactive
-  double sa[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, sq2[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-  // (the register-capped two-CTA build keeps one column per thread over all 256 threads: the pair form
-  // spills there, n = 64 355 -> 310 GB/s)
-  constexpr bool kPairStats = kPreload;
   double l1a[2] = {0.0, 0.0}, sqa[2] = {0.0, 0.0};
 
   for (int64_t r0 = 0; r0 < nrows; r0 += brows) {
@@ -611,7 +600,7 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
-    if (!kPairStats && stats_out) {
+    if (stats_out) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int col = tid + h * kTqThreads;
@@ -624,26 +613,6 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
           }
           l1a[h] = a;
           sqa[h] = q;
-        }
-      }
-    }
-    if (kPairStats && stats_out && st_ph < nph) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int pr = st_pair + h * 224;
-        if ((h == 0 || npairs > 224) && pr < npairs && 2 * pr < ncols) {
-          double a0 = sa[h][0], a1 = sa[h][1], q0 = sq2[h][0], q1 = sq2[h][1];
-          for (int i = st_ph; i < cnt; i += nph) {
-            const double2 v = *reinterpret_cast<const double2*>(Bs + i * lds + ((2 * pr) ^ swz(i)));
-            a0 += fabs(v.x);
-            a1 += fabs(v.y);
-            q0 = fma(v.x, v.x, q0);
-            q1 = fma(v.y, v.y, q1);
-          }
-          sa[h][0] = a0;
-          sa[h][1] = a1;
-          sq2[h][0] = q0;
-          sq2[h][1] = q1;
         }
       }
     }
@@ -714,7 +683,7 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
       }
     }
   }
-  if (!kPairStats && stats_out) {
+  if (stats_out) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int col = tid + h * kTqThreads;
@@ -722,34 +691,6 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
         stats_out[col] = l1a[h];
         stats_out[npad + col] = sqa[h];
       }
-    }
-  }
-  if (kPairStats && stats_out) {  // fixed-order sum of the row phases through shared memory (block area free)
-    __syncthreads();
-    double* ps = smem;  // [phase][2][npad]
-    for (int idx = tid; idx < nph * 2 * npad; idx += kTqThreads) ps[idx] = 0.0;
-    __syncthreads();
-    if (st_ph < nph) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int pr = st_pair + h * 224;
-        if ((h == 0 || npairs > 224) && pr < npairs) {
-          ps[(st_ph * 2 + 0) * npad + 2 * pr] = sa[h][0];
-          ps[(st_ph * 2 + 0) * npad + 2 * pr + 1] = sa[h][1];
-          ps[(st_ph * 2 + 1) * npad + 2 * pr] = sq2[h][0];
-          ps[(st_ph * 2 + 1) * npad + 2 * pr + 1] = sq2[h][1];
-        }
-      }
-    }
-    __syncthreads();
-    for (int c = tid; c < npad; c += kTqThreads) {
-      double a = 0.0, q = 0.0;
-      for (int r = 0; r < nph; ++r) {
-        a += ps[(r * 2 + 0) * npad + c];
-        q += ps[(r * 2 + 1) * npad + c];
-      }
-      stats_out[c] = a;
-      stats_out[npad + c] = q;
     }
   }
 }
