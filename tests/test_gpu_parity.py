@@ -382,3 +382,14 @@ def test_magnitude_range(oracle, n):
     for scale in (1e-170, 1e170):
         with pytest.raises(tb.NumericalError):
             tb.stream_pass([tb.RowChunk(0, dev(x * scale))])
+
+
+@pytest.mark.parametrize("m,n", [(235, 235), (1000, 235), (5000, 240), (300, 100), (777, 64), (4097, 200)])
+def test_column_stats_every_block_size(m, n):
+    """The fused column stats read the staged block while the panel warp starts factoring it; every
+    width / block-size combination must see the unmodified data (a column-pair variant that let other
+    warps read panel 0's columns raced with the panel's write-back: n=235 l1 off by ~1% on columns 0-7)."""
+    x = np.random.default_rng(m + n).standard_normal((m, n))
+    _, l1, sq = dv.tsqr(dev(x))
+    np.testing.assert_allclose(l1.cpu().numpy(), np.abs(x).sum(0), rtol=1e-12)
+    np.testing.assert_allclose(sq.cpu().numpy(), (x * x).sum(0), rtol=1e-12)
