@@ -553,12 +553,18 @@ __device__ __forceinline__ void lookahead_pair(double* __restrict__ Bs, int lds,
 //   GEMM warps : wait PanelDone(p) -> arrive ColsReady(p+1) -> update column blocks p+2.. with panel p
 // so panel p+1 is factored while the trailing update of panel p runs.  V_p lives in the block's
 // panel-p columns (never touched again this block); T and the staged R rows are double-buffered.
-template <int RQ, bool kPreload>
+template <int RQ, bool kPreload, int W = kTqWarps>
 __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src, int64_t nrows, int64_t ldsrc,
                           int ncols, const TqGeom g, bool triangular, bool init_zero,
                           double* __restrict__ stats_out, double* smem) {
   using L = TqLayout;
   constexpr int G = 4;  // column blocks per GEMM group
+  // W = 8: panel warp 0, helper warp 4 (both SMSP 0), six GEMM warps.  W = 4 (three CTAs per SM, n <= 64):
+  // panel warp 0, helper warp 2, GEMM warps 1 and 3.
+  constexpr int kThr = 32 * W;
+  constexpr int kHelper = W == 8 ? 4 : 2;
+  constexpr int kGemm = W - 2;
+  constexpr int kSH = (512 + kThr - 1) / kThr;  // stats columns per thread (n <= 512)
   const int tid = threadIdx.x, lane = tid & 31;
   int warp = tid >> 5;  // logical warp (role); physical warp = (warp + rot) % 8
   if constexpr (!kPreload) {
@@ -576,6 +582,18 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
     __syncthreads();
     warp = (warp - *s_rot) & (kTqWarps - 1);
   }
+  if constexpr (W == 4) {
+    // three 4-warp CTAs per SM occupy hardware slots 0-3, 4-7, 8-11: rotate the roles by the CTA's slot
+    // group so the three panel warps run on different SMSPs (a hint only)
+    volatile int* s_rot = reinterpret_cast<volatile int*>(smem + TqLayout::red(g));
+    if (tid == 0) {
+      unsigned wid;
+      asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+      *s_rot = (int)((wid >> 2) & 3u);
+    }
+    __syncthreads();
+    warp = (warp - *s_rot) & (W - 1);
+  }
   const int npad = g.npad, lds = g.lds, brows = g.brows;
   double* Bs = smem;
   double* Rdg = smem + L::rd(g);
@@ -587,9 +605,11 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
   const bool vec16 = ((ldsrc & 1) == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
 
   if (init_zero) {
-    for (int64_t idx = tid; idx < (int64_t)npad * npad; idx += kTqThreads) R[idx] = 0.0;
+    for (int64_t idx = tid; idx < (int64_t)npad * npad; idx += kThr) R[idx] = 0.0;
   }
-  double l1a[2] = {0.0, 0.0}, sqa[2] = {0.0, 0.0};
+  double l1a[kSH], sqa[kSH];
+#pragma unroll
+  for (int h = 0; h < kSH; ++h) l1a[h] = sqa[h] = 0.0;
 
   for (int64_t r0 = 0; r0 < nrows; r0 += brows) {
     const int cnt = (int)min64(brows, nrows - r0);
@@ -602,8 +622,8 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
     __syncthreads();
     if (stats_out) {
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int col = tid + h * kTqThreads;
+      for (int h = 0; h < kSH; ++h) {
+        const int col = tid + h * kThr;
         if (col < ncols) {
           double a = l1a[h], q = sqa[h];
           for (int i = 0; i < cnt; ++i) {
@@ -624,20 +644,20 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
       const bool more = p + 1 < npanels;
       const int tq_p = (r0 == 0 && p < 64) ? p : -1;
       if (warp == 0) {
-        if (p > p0) named_sync(kBarColsReady, kTqThreads);
+        if (p > p0) named_sync(kBarColsReady, kThr);
         TQ_RESOLVE(Rdg);
         TQ_TRACE(1);
         panel_factor_lazy<RQ, kPreload>(Bs, lds, brows, j0, R, npad, Rdc, Tm + buf * kNB * kNB, red, lane, tq_p);
         TQ_TRACE(2);
-        named_arrive(kBarPanelDone, kTqThreads);
+        named_arrive(kBarPanelDone, kThr);
         if (kPairLookahead && more) {
           __syncwarp();  // the warp's own V / T stores are visible to all its lanes
           lookahead_pair(Bs, lds, brows, j0, R, npad, Tmc, Wpart, Wsc, p + 1, 0, lane);
         }
-      } else if (warp == 4) {
+      } else if (warp == kHelper) {
         // helper on SMSP 0: the lookahead starts the moment the panel is published (not after the GEMM
         // warps' trailing work) and its DMMAs never overlap the panel's FP64 chain on this SMSP
-        named_sync(kBarPanelDone, kTqThreads);
+        named_sync(kBarPanelDone, kThr);
         TQ_RESOLVE(Rdg);
         if (more) {
           TQ_TRACE(3);
@@ -650,20 +670,20 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
           cp_async_wait<0>();
           __syncwarp();
           TQ_TRACE(4);
-          named_arrive(kBarColsReady, kTqThreads);
+          named_arrive(kBarColsReady, kThr);
         }
       } else {
-        const int gi = gemm_index(warp);
-        named_sync(kBarPanelDone, kTqThreads);
+        const int gi = W == 8 ? gemm_index(warp) : (warp == 1 ? 0 : 1);
+        named_sync(kBarPanelDone, kThr);
         TQ_RESOLVE(Rdg);
-        if (more) named_arrive(kBarColsReady, kTqThreads);
+        if (more) named_arrive(kBarColsReady, kThr);
         // trailing column blocks p+2 .. ncb-1, round-robin over the GEMM warps in groups of G
-        for (int base = p + 2 + gi; base < ncb; base += kGemmWarps * G) {
+        for (int base = p + 2 + gi; base < ncb; base += kGemm * G) {
           int cnt_g = 0;
           int cbs[G];
 #pragma unroll
           for (int gg = 0; gg < G; ++gg) {
-            cbs[gg] = base + kGemmWarps * gg;
+            cbs[gg] = base + kGemm * gg;
             if (cbs[gg] < ncb) ++cnt_g;
           }
           // a short last group is updated in one call (shared V fragment loads), not block by block
@@ -685,8 +705,8 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
   }
   if (stats_out) {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int col = tid + h * kTqThreads;
+    for (int h = 0; h < kSH; ++h) {
+      const int col = tid + h * kThr;
       if (col < npad) {
         stats_out[col] = l1a[h];
         stats_out[npad + col] = sqa[h];
@@ -695,8 +715,12 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
   }
 }
 
+// MINB == 3 selects the 4-warp CTA (three per SM, n <= 64)
+template <int MINB>
+constexpr int tq_warps() { return MINB == 3 ? 4 : kTqWarps; }
+
 template <int RQ, int MINB>
-__global__ void __launch_bounds__(kTqThreads, MINB)
+__global__ void __launch_bounds__(32 * tq_warps<MINB>(), MINB)
     tsqr_leaf_kernel(const double* __restrict__ x, int64_t m, int64_t ldx, int64_t rows_per_cta, TqGeom g,
                      double* __restrict__ slots, double* __restrict__ stats) {
   extern __shared__ __align__(16) double smem[];
@@ -704,13 +728,13 @@ __global__ void __launch_bounds__(kTqThreads, MINB)
   const int64_t cnt = max64(0, min64(rows_per_cta, m - r0));
   double* R = slots + (int64_t)blockIdx.x * g.npad * g.npad;
   double* st = stats ? stats + (int64_t)blockIdx.x * 2 * g.npad : nullptr;
-  tsqr_fold<RQ, MINB == 1>(R, x + r0 * ldx, cnt, ldx, g.n, g, false, true, st, smem);
+  tsqr_fold<RQ, MINB != 2, tq_warps<MINB>()>(R, x + r0 * ldx, cnt, ldx, g.n, g, false, true, st, smem);
 }
 
 // One level of the binary-counter tree: slot[q*2^L] = qr([slot[q*2^L]; slot[q*2^L + 2^(L-1)]]),
 // or (fold) slot[dst] = qr([slot[dst]; slot[src]]).
 template <int RQ, int MINB>
-__global__ void __launch_bounds__(kTqThreads, MINB)
+__global__ void __launch_bounds__(32 * tq_warps<MINB>(), MINB)
     tsqr_combine_kernel(double* __restrict__ slots, int64_t span, int64_t half, int64_t fold_dst, int64_t fold_src,
                         TqGeom g) {
   extern __shared__ __align__(16) double smem[];
@@ -723,7 +747,8 @@ __global__ void __launch_bounds__(kTqThreads, MINB)
     dst = fold_dst;
     srcs = fold_src;
   }
-  tsqr_fold<RQ, MINB == 1>(slots + dst * ss, slots + srcs * ss, g.npad, g.npad, g.npad, g, true, false, nullptr, smem);
+  tsqr_fold<RQ, MINB != 2, tq_warps<MINB>()>(slots + dst * ss, slots + srcs * ss, g.npad, g.npad, g.npad, g, true, false,
+                                              nullptr, smem);
 }
 
 // ---------------------------------------------------------------------------
@@ -1189,7 +1214,7 @@ bool tq_choose(int n, int minb, TqChoice* out) {
   g.n = n;
   g.npad = (int)round_up(n, kNB);
   g.lds = smem_stride(g.npad);
-  const size_t budget = (minb == 2 ? 113 : 226) * 1024;
+  const size_t budget = (minb == 3 ? 74 : (minb == 2 ? 113 : 226)) * 1024;
   int best = 0;
   // multiple of 16 (B -= V W' runs row-block pairs; 136 rows at n = 200 with an odd-block tail measured
   // slower, 228 vs 234 GB/s); above 128 rows (RQ = 5) only for the one-CTA build at n > 64, whose register
@@ -1213,10 +1238,13 @@ bool tq_config(int n, TqChoice* out) {
   // Occupancy: the throughput is (rows in flight) / (n x per-column panel latency) per panel chain (see
   // DESIGN.md).  Narrow matrices (n <= 64) fit a full 128-row block in half the shared memory, so two CTAs
   // per SM give two independent panel chains (measured +50% at n = 25 and 64); wider ones run one CTA
-  // with the largest block.  TSNMF_TSQR_CTAS=1/2 overrides for tuning.
-  int minb = n <= 64 ? 2 : 1;
-  if (const char* e = getenv("TSNMF_TSQR_CTAS")) minb = atoi(e) == 2 ? 2 : 1;
-  if (minb == 2 && tq_choose(n, 2, out) && out->g.brows >= (n <= 64 ? 128 : 48)) return true;
+  // with the largest block.  TSNMF_TSQR_CTAS=1/2/3 overrides for tuning.
+  // n <= 64: three 4-warp CTAs per SM (three panel chains, 112-row blocks, 168 registers: measured n=64
+  // 355 -> 406, n=48 370 -> 476 GB/s vs two 8-warp CTAs, whose 128-register cap forces spills)
+  int minb = n <= 64 ? 3 : 1;
+  if (const char* e = getenv("TSNMF_TSQR_CTAS")) minb = atoi(e) == 3 ? 3 : (atoi(e) == 2 ? 2 : 1);
+  if (minb == 3 && n <= 64 && tq_choose(n, 3, out) && out->g.brows >= 64) return true;
+  if (minb >= 2 && tq_choose(n, 2, out) && out->g.brows >= (n <= 64 ? 128 : 48)) return true;
   return tq_choose(n, 1, out);
 }
 
@@ -1233,7 +1261,7 @@ int tq_launch_all(const TqChoice& ch, const double* x, int64_t m, int64_t ldx, d
   }
   if (x) {
     prof_mark(kProfTsqrLeaf, true, st);
-    tsqr_leaf_kernel<RQ, MINB><<<nleaves, kTqThreads, ch.smem, st>>>(x, m, ldx, rows_per_cta, ch.g, slots, stats);
+    tsqr_leaf_kernel<RQ, MINB><<<nleaves, 32 * tq_warps<MINB>(), ch.smem, st>>>(x, m, ldx, rows_per_cta, ch.g, slots, stats);
     TSNMF_LAUNCH_CHECK();
     prof_mark(kProfTsqrLeaf, false, st);
   }
@@ -1241,7 +1269,7 @@ int tq_launch_all(const TqChoice& ch, const double* x, int64_t m, int64_t ldx, d
   // binary-counter tree (tsqr.py:213-230): perfect levels, then fold leftover subtrees low -> high
   for (int64_t span = 2; span <= nleaves; span *= 2) {
     const int64_t q = nleaves / span;
-    tsqr_combine_kernel<RQ, MINB><<<(unsigned)q, kTqThreads, ch.smem, st>>>(slots, span, span / 2, 0, 0, ch.g);
+    tsqr_combine_kernel<RQ, MINB><<<(unsigned)q, 32 * tq_warps<MINB>(), ch.smem, st>>>(slots, span, span / 2, 0, 0, ch.g);
     TSNMF_LAUNCH_CHECK();
   }
   int64_t offs[64];
@@ -1253,7 +1281,7 @@ int tq_launch_all(const TqChoice& ch, const double* x, int64_t m, int64_t ldx, d
       o += (1LL << b);
     }
   for (int t = nsub - 2; t >= 0; --t) {
-    tsqr_combine_kernel<RQ, MINB><<<1, kTqThreads, ch.smem, st>>>(slots, 0, 0, offs[t], offs[t + 1], ch.g);
+    tsqr_combine_kernel<RQ, MINB><<<1, 32 * tq_warps<MINB>(), ch.smem, st>>>(slots, 0, 0, offs[t], offs[t + 1], ch.g);
     TSNMF_LAUNCH_CHECK();
   }
   prof_mark(kProfTsqrTree, false, st);
@@ -1276,6 +1304,7 @@ int tq_dispatch_rq(const TqChoice& ch, const double* x, int64_t m, int64_t ldx, 
 
 int tq_dispatch(const TqChoice& ch, const double* x, int64_t m, int64_t ldx, double* slots, double* stats,
                 int nleaves, int64_t rows_per_cta, cudaStream_t st) {
+  if (ch.minb == 3) return tq_dispatch_rq<3>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
   if (ch.minb == 2) return tq_dispatch_rq<2>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
   return tq_dispatch_rq<1>(ch, x, m, ldx, slots, stats, nleaves, rows_per_cta, st);
 }
