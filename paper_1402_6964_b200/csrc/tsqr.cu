@@ -1239,11 +1239,12 @@ bool tq_config(int n, TqChoice* out) {
   // DESIGN.md).  Narrow matrices (n <= 64) fit a full 128-row block in half the shared memory, so two CTAs
   // per SM give two independent panel chains (measured +50% at n = 25 and 64); wider ones run one CTA
   // with the largest block.  TSNMF_TSQR_CTAS=1/2/3 overrides for tuning.
-  // n <= 64: three 4-warp CTAs per SM (three panel chains, 112-row blocks, 168 registers: measured n=64
-  // 355 -> 406, n=48 370 -> 476 GB/s vs two 8-warp CTAs, whose 128-register cap forces spills)
-  int minb = n <= 64 ? 3 : 1;
+  // n <= 96: three 4-warp CTAs per SM (three panel chains, 64-112-row blocks, 168 registers): measured
+  // n=48 370 -> 476, n=64 355 -> 406 (vs two 8-warp CTAs, whose 128-register cap forces spills), n=72
+  // 273 -> 388, n=96 272 -> 328 GB/s (vs one 8-warp CTA); n=128 is better with one CTA (270 vs 237)
+  int minb = n <= 104 ? 3 : 1;  // (97..104 have n = 96's padded width and shared-memory footprint)
   if (const char* e = getenv("TSNMF_TSQR_CTAS")) minb = atoi(e) == 3 ? 3 : (atoi(e) == 2 ? 2 : 1);
-  if (minb == 3 && n <= 64 && tq_choose(n, 3, out) && out->g.brows >= 64) return true;
+  if (minb == 3 && n <= 128 && tq_choose(n, 3, out) && out->g.brows >= 48) return true;
   if (minb >= 2 && tq_choose(n, 2, out) && out->g.brows >= (n <= 64 ? 128 : 48)) return true;
   return tq_choose(n, 1, out);
 }
