@@ -91,5 +91,15 @@ def check(status: int, stage: str = "device") -> None:
     raise cls(msg, stage=stage)
 
 
-def call(name: str, *args, stage: str = "device") -> None:
-    check(getattr(load(), name)(*args), stage=stage)
+def call(name: str, *args, stage: str = "device", device=None) -> None:
+    """Call one C-ABI entry point.  With ``device`` the call runs with that CUDA device current: the
+    library launches on the stream it is given but sets per-device kernel attributes and queries the
+    SM count of the *current* device, so the two must agree."""
+    fn = getattr(load(), name)
+    if device is None:
+        check(fn(*args), stage=stage)
+        return
+    import torch
+
+    with torch.cuda.device(device):
+        check(fn(*args), stage=stage)

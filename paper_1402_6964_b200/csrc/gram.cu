@@ -256,11 +256,11 @@ size_t gram_workspace_bytes(int64_t m, int n) {
 template <int SPW, int WARPS>
 int gram_launch(const double* x, int64_t m, int64_t ldx, const GrGeom& g, double* partial, double* l1part,
                 int64_t splits, size_t smem, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceFlag attr;
+  if (!attr.is_set()) {
     TSNMF_CUDA_CHECK((cudaFuncSetAttribute(gram_kernel<SPW, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            232448)));
-    attr = true;
+    attr.set();
   }
   gram_kernel<SPW, WARPS><<<dim3(g.groups, (unsigned)splits), 32 * WARPS, smem, st>>>(x, m, ldx, g, partial, l1part);
   TSNMF_LAUNCH_CHECK();

@@ -5,9 +5,27 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 
 namespace tsnmf {
+
+// cudaFuncSetAttribute (the >48 KB dynamic shared-memory opt-in) applies to the CURRENT device only, so a
+// launcher remembers per device whether it has set its kernels' attributes (a process-wide flag
+// left every GPU but the first without the opt-in).
+class PerDeviceFlag {
+ public:
+  bool is_set() const { return (bits_.load(std::memory_order_acquire) >> dev()) & 1u; }
+  void set() { bits_.fetch_or(1ull << dev(), std::memory_order_acq_rel); }
+
+ private:
+  static int dev() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d & 63;
+  }
+  std::atomic<unsigned long long> bits_{0};
+};
 
 int set_error(int status, const char* fmt, ...);
 

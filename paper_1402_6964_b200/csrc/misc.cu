@@ -154,10 +154,10 @@ int generate_run(double* x, int64_t ldx, int64_t row0, int64_t rows, int n, int 
   const dim3 block(32, 8);
   const size_t smem = sizeof(double) * (size_t)(r * n + 8 * r);
   if (smem > 200 * 1024) return set_error(kUsage, "generate: r * n too large");
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceFlag attr;
+  if (!attr.is_set()) {
     TSNMF_CUDA_CHECK(cudaFuncSetAttribute(generate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
-    attr = true;
+    attr.set();
   }
   generate_kernel<<<(unsigned)ceil_div(rows, 8), block, smem, st>>>(x, ldx, row0, rows, n, r, mix, w_kind, bumps,
                                                                    m_total, sigma, derive_stream(seed, kTagCfgW),

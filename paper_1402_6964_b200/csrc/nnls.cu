@@ -247,10 +247,10 @@ int nnls_run(const double* a, int64_t n, int t, int64_t lda, const double* b, in
   nnls_gram_kernel<<<(unsigned)ceil_div(t * t, 128), 128, 0, st>>>(a, n, t, lda, g);
   TSNMF_LAUNCH_CHECK();
   const size_t smem = sizeof(double) * (2 * kNnlsMaxT * kNnlsMaxT + 4 * kNnlsMaxT) + sizeof(int) * kNnlsMaxT;
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceFlag attr;
+  if (!attr.is_set()) {
     TSNMF_CUDA_CHECK(cudaFuncSetAttribute(nnls_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
+    attr.set();
   }
   nnls_solve_kernel<<<ncols, 32, smem, st>>>(a, n, t, lda, b, ldb, ncols, g, tol, max_iter, y, ldy, status);
   TSNMF_LAUNCH_CHECK();

@@ -1252,13 +1252,13 @@ bool tq_config(int n, TqChoice* out) {
 template <int RQ, int MINB>
 int tq_launch_all(const TqChoice& ch, const double* x, int64_t m, int64_t ldx, double* slots, double* stats,
                   int nleaves, int64_t rows_per_cta, cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  static PerDeviceFlag attr_set;
+  if (!attr_set.is_set()) {
     TSNMF_CUDA_CHECK(cudaFuncSetAttribute(tsqr_leaf_kernel<RQ, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           232448));
     TSNMF_CUDA_CHECK(cudaFuncSetAttribute(tsqr_combine_kernel<RQ, MINB>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
-    attr_set = true;
+    attr_set.set();
   }
   if (x) {
     prof_mark(kProfTsqrLeaf, true, st);
@@ -1311,11 +1311,14 @@ int tq_dispatch(const TqChoice& ch, const double* x, int64_t m, int64_t ldx, dou
 }
 
 int device_sms() {
-  static int sms = 0;
+  static std::atomic<int> sms_of[64];  // per device (0 = not queried yet)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::atomic<int>& slot = sms_of[dev & 63];
+  int sms = slot.load(std::memory_order_relaxed);
   if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = kNumSMs;
+    slot.store(sms, std::memory_order_relaxed);
   }
   return sms;
 }
@@ -1457,11 +1460,11 @@ int warp_leaf(const double* x, int64_t m, int n, int64_t ldx, int64_t rpw, int n
 template <int NC>
 int small_launch(const double* x, int64_t m, int n, int64_t ldx, int64_t rpw, int nleaves, int npad, double* slots,
                  double* stats, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceFlag attr;
+  if (!attr.is_set()) {
     TSNMF_CUDA_CHECK(cudaFuncSetAttribute(tsqr_small_leaf_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)SmallLayout<NC>::bytes));
-    attr = true;
+    attr.set();
   }
   prof_mark(kProfTsqrLeaf, true, st);
   tsqr_small_leaf_kernel<NC><<<nleaves / kSmWarps, 32 * kSmWarps, SmallLayout<NC>::bytes, st>>>(

@@ -128,7 +128,7 @@ def tsqr(x, *, stats: bool = True):
     ws, wsb = _workspace(_native.OP_TSQR, m, n, 0, dev)
     _native.call("tsnmf_tsqr", x.data_ptr(), m, n, _ld(x), r.data_ptr(), n,
                  l1.data_ptr() if stats else None, sq.data_ptr() if stats else None, ws, wsb,
-                 stream_ptr(dev), stage="tsqr")
+                 stream_ptr(dev), device=dev, stage="tsqr")
     return r, l1, sq
 
 
@@ -141,7 +141,7 @@ def combine_factors(rs):
     dev = rs.device
     r = t.empty((n, n), dtype=t.float64, device=dev)
     ws, wsb = _workspace(_native.OP_COMBINE, count, n, 0, dev)
-    _native.call("tsnmf_r_combine", rs.data_ptr(), count, n, r.data_ptr(), n, ws, wsb, stream_ptr(dev),
+    _native.call("tsnmf_r_combine", rs.data_ptr(), count, n, r.data_ptr(), n, ws, wsb, stream_ptr(dev), device=dev,
                  stage="combine")
     return r
 
@@ -158,7 +158,7 @@ def gram(x, *, stats: bool = True):
     ws, wsb = _workspace(_native.OP_GRAM, m, n, 0, dev)
     _native.call("tsnmf_gram", x.data_ptr(), m, n, _ld(x), g.data_ptr(), n,
                  l1.data_ptr() if stats else None, sq.data_ptr() if stats else None, ws, wsb,
-                 stream_ptr(dev), stage="gram")
+                 stream_ptr(dev), device=dev, stage="gram")
     return g, l1, sq
 
 
@@ -179,7 +179,7 @@ def sketch(x, row_offset: int, seed: int, k: int, g=None):
         gp, ldg = g.data_ptr(), _ld(g) if m > 1 else k
     ws, wsb = _workspace(_native.OP_SKETCH, m, n, k, dev)
     _native.call("tsnmf_sketch", x.data_ptr(), m, n, _ld(x), int(row_offset), int(seed) & ((1 << 64) - 1), int(k),
-                 gp, ldg, s.data_ptr(), n, ws, wsb, stream_ptr(dev), stage="sketch")
+                 gp, ldg, s.data_ptr(), n, ws, wsb, stream_ptr(dev), device=dev, stage="sketch")
     return s
 
 
@@ -192,7 +192,7 @@ def column_stats(x):
     sq = t.empty(n, dtype=t.float64, device=dev)
     ws, wsb = _workspace(_native.OP_STATS, m, n, 0, dev)
     _native.call("tsnmf_column_stats", x.data_ptr(), m, n, _ld(x), l1.data_ptr(), sq.data_ptr(), ws, wsb,
-                 stream_ptr(dev), stage="stats")
+                 stream_ptr(dev), device=dev, stage="stats")
     return l1, sq
 
 
@@ -204,7 +204,7 @@ def first_nonfinite(x) -> int:
         raise UsageError("first_nonfinite needs a contiguous CUDA float64 tensor")
     dev = x.device
     out = t.empty(1, dtype=t.int64, device=dev)
-    _native.call("tsnmf_first_nonfinite", x.data_ptr(), int(x.numel()), out.data_ptr(), stream_ptr(dev),
+    _native.call("tsnmf_first_nonfinite", x.data_ptr(), int(x.numel()), out.data_ptr(), stream_ptr(dev), device=dev,
                  stage="read")
     return int(out.item())
 
@@ -229,7 +229,7 @@ def nnls(a, b, *, tol: float = 1e-8, max_iter: int = 10_000):
     status = t.empty(ncols, dtype=t.int32, device=dev)
     ws, wsb = _workspace(_native.OP_NNLS, 1, q, 0, dev)
     _native.call("tsnmf_nnls", a.data_ptr(), n, q, _ld(a), b.data_ptr(), _ld(b), ncols, float(tol), int(max_iter),
-                 y.data_ptr(), ncols, status.data_ptr(), ws, wsb, stream_ptr(dev), stage="nnls")
+                 y.data_ptr(), ncols, status.data_ptr(), ws, wsb, stream_ptr(dev), device=dev, stage="nnls")
     return y, status
 
 
@@ -243,7 +243,7 @@ def xray_scores(m, resid, colnorm):
     n = int(m.shape[0])
     score = t.empty(n, dtype=t.float64, device=m.device)
     _native.call("tsnmf_xray_scores", m.data_ptr(), n, _ld(m), resid.data_ptr(), _ld(resid), colnorm.data_ptr(),
-                 score.data_ptr(), stream_ptr(m.device), stage="xray")
+                 score.data_ptr(), stream_ptr(m.device), device=m.device, stage="xray")
     return score
 
 
@@ -251,7 +251,7 @@ def xray_residual(m, a, coef, out):
     """out = m - a @ coef (reference select.py:138-140)."""
     n, q = int(m.shape[0]), int(a.shape[1])
     _native.call("tsnmf_xray_residual", m.data_ptr(), n, _ld(m), a.data_ptr(), q, _ld(a), coef.data_ptr(),
-                 _ld(coef), out.data_ptr(), _ld(out), stream_ptr(m.device), stage="xray")
+                 _ld(coef), out.data_ptr(), _ld(out), stream_ptr(m.device), device=m.device, stage="xray")
     return out
 
 
@@ -264,7 +264,7 @@ def uniform_block(stream: int, start: int, count: int, device=None):
     dev = require_device(device)
     out = t.empty(int(count), dtype=t.float64, device=dev)
     _native.call("tsnmf_uniform_block", int(stream) & ((1 << 64) - 1), int(start) & ((1 << 64) - 1), int(count),
-                 out.data_ptr(), stream_ptr(dev), stage="rng")
+                 out.data_ptr(), stream_ptr(dev), device=dev, stage="rng")
     return out
 
 
@@ -273,7 +273,7 @@ def normal_block(stream: int, start: int, count: int, device=None):
     dev = require_device(device)
     out = t.empty(int(count), dtype=t.float64, device=dev)
     _native.call("tsnmf_normal_block", int(stream) & ((1 << 64) - 1), int(start) & ((1 << 64) - 1), int(count),
-                 out.data_ptr(), stream_ptr(dev), stage="rng")
+                 out.data_ptr(), stream_ptr(dev), device=dev, stage="rng")
     return out
 
 
@@ -282,7 +282,7 @@ def gaussian_rows(seed: int, row_offset: int, rows: int, k: int, device=None):
     dev = require_device(device)
     out = t.empty((int(rows), int(k)), dtype=t.float64, device=dev)
     _native.call("tsnmf_gaussian_rows", int(seed) & ((1 << 64) - 1), int(row_offset), int(rows), int(k),
-                 out.data_ptr(), stream_ptr(dev), stage="rng")
+                 out.data_ptr(), stream_ptr(dev), device=dev, stage="rng")
     return out
 
 

@@ -6,16 +6,19 @@ Semantics kept from the reference:
   * ``TriangularFactor`` / ``ColumnStats`` / ``ReducedSVD`` / ``StreamResult``
     validation and read-only arrays (tsqr.py:27-110, 237-244);
   * ``combine_order``: "tree" (binary-counter tree over the chunk index,
-    deterministic), "sequential" (left fold), "first-come" (accepted; on the
-    device the order is deterministic anyway) (tsqr.py:24, 294-333);
+    deterministic), "sequential" (left fold), "first-come" (tree with
+    threads == 1, as in the reference; a left fold in arrival order with
+    threads > 1) (tsqr.py:24, 294-333);
   * errors: empty stream -> DataError, m < n -> DataError("not tall-and-skinny"),
     bad order / threads -> UsageError (tsqr.py:294-297, 335-341).
 
 What changes: every chunk is reduced by ``libtsnmf_b200.so`` (device.py).
 Device-resident chunks (torch CUDA float64) are reduced in place; host chunks
-(numpy) are gathered into large pinned batches that stream over PCIe while the
-previous batch is being reduced.  ``threads`` is accepted for signature
-compatibility only.
+(numpy) are gathered into ~1 GiB batches: pageable pieces are first packed into
+one of two reusable pinned staging buffers (already-pinned pieces are copied
+directly), and each batch's H2D copy runs on a side stream while the previous
+batch is being reduced.  ``threads`` is accepted for signature compatibility
+(and, as in the reference, selects the fold order of "first-come").
 """
 
 from __future__ import annotations
@@ -416,6 +419,7 @@ def _reduce_host(chunks, engine: _PassEngine, dev):
     copy_stream = t.cuda.Stream(dev)
     compute_stream = t.cuda.current_stream(dev)
     bufs: list = [None, None]
+    stage: list = [None, None]  # pinned host staging buffers (pageable pieces are packed here first)
     done_ev: list = [None, None]
     ready_ev: list = [None, None]
     hold: list = [None, None]  # host sources of in-flight copies
@@ -426,20 +430,34 @@ def _reduce_host(chunks, engine: _PassEngine, dev):
         n = pieces[0][1].shape[1]
         buf = bufs[slot]
         if buf is None or buf.shape[1] != n or buf.shape[0] < rows:
-            buf = t.empty((max(rows, batch_rows(n)), n), dtype=t.float64, device=dev)
+            buf = t.empty((max(rows, min(batch_rows(n), 2 * rows)), n), dtype=t.float64, device=dev)
             bufs[slot] = buf
         if ready_ev[slot] is not None:
-            ready_ev[slot].synchronize()  # copies two batches ago done: release their sources
+            ready_ev[slot].synchronize()  # copies two batches ago done: release their sources / staging
         hold[slot] = []
+        srcs = [t.from_numpy(np.ascontiguousarray(arr)) for _, arr in pieces]
+        pinned = all(s.is_pinned() for s in srcs)
+        if not pinned:
+            # a copy from pageable memory is staged by the driver and is effectively synchronous, so pack
+            # the batch into a reusable pinned buffer: the H2D below then overlaps the previous reduction
+            st = stage[slot]
+            if st is None or st.shape[1] != n or st.shape[0] < rows:
+                st = t.empty((buf.shape[0], n), dtype=t.float64, pin_memory=True)
+                stage[slot] = st
+            st_np = st.numpy()
+            pos = 0
+            for _, arr in pieces:
+                st_np[pos:pos + arr.shape[0]] = arr
+                pos += arr.shape[0]
+            srcs = [st[:rows]]
         with t.cuda.stream(copy_stream):
             if done_ev[slot] is not None:
                 copy_stream.wait_event(done_ev[slot])
             pos = 0
-            for _, arr in pieces:
-                src = t.from_numpy(np.ascontiguousarray(arr))
+            for src in srcs:
                 hold[slot].append(src)
-                buf[pos:pos + arr.shape[0]].copy_(src, non_blocking=True)
-                pos += arr.shape[0]
+                buf[pos:pos + src.shape[0]].copy_(src, non_blocking=True)
+                pos += src.shape[0]
             ready = t.cuda.Event()
             ready.record(copy_stream)
         ready_ev[slot] = ready
@@ -452,12 +470,15 @@ def _reduce_host(chunks, engine: _PassEngine, dev):
         slot ^= 1
 
 
-def _run_pass(chunks, engine: _PassEngine, combine_order: str):
+def _run_pass(chunks, engine: _PassEngine, combine_order: str, threads: int = 1):
     if combine_order not in COMBINE_ORDERS:
         raise UsageError(f"combine_order must be one of {COMBINE_ORDERS}")
     n_chunks = 0
     depth = 0
-    if combine_order == "tree":
+    # reference tsqr.py:315-333: "first-come" folds in completion order only with threads > 1 (one
+    # completion order of a deterministic device pass is the input order); with threads == 1 it takes the
+    # ordered-map branch, i.e. the tree, and reports the tree depth
+    if combine_order == "tree" or (combine_order == "first-come" and threads <= 1):
         red = TreeReducer(_merge_nodes)
         for node, consumed in _iter_nodes(chunks, engine):
             n_chunks += consumed
@@ -499,7 +520,8 @@ def stream_pass(chunks: Iterable[RowChunk], *, sketch_rows: int | None = None, s
         raise UsageError(f"threads must be >= 1, got {threads}")
     if sketch_rows is not None and sketch_rows < 1:
         raise UsageError(f"sketch rows must be >= 1, got {sketch_rows}")
-    node, n_chunks, depth = _run_pass(chunks, _PassEngine(True, sketch_rows, seed, False), combine_order)
+    node, n_chunks, depth = _run_pass(chunks, _PassEngine(True, sketch_rows, seed, False), combine_order,
+                                      threads)
     if node.rows < node.n:
         raise DataError(f"not tall-and-skinny: m = {node.rows} < n = {node.n}")
     l1, sq = node.l1.cpu().numpy(), node.sq.cpu().numpy()

@@ -93,7 +93,7 @@ def generate_into(out, spec: ConfigSpec, row0: int = 0, mix=None, bumps=None):
         _native.call("tsnmf_generate", view.data_ptr(), int(out.stride(0)), int(row0 + a), int(b - a), spec.n,
                      spec.r, mix_d.data_ptr(), _W_KIND[spec.w_kind],
                      bumps_d.data_ptr() if bumps_d is not None else None, int(spec.m), float(spec.sigma),
-                     int(spec.seed), dv.stream_ptr(dev), stage="generate")
+                     int(spec.seed), dv.stream_ptr(dev), device=dev, stage="generate")
     return out
 
 

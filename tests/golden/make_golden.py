@@ -77,7 +77,8 @@ def tsqr_fixture(ts):
     for name, x in small_cases().items():
         out[f"{name}__x"] = x
         for size in (1, 7, 64, x.shape[0]):
-            for order in ("tree", "sequential"):
+            # "first-come" with threads=1 takes the reference's ordered tree branch (tsqr.py:315-333)
+            for order in ("tree", "sequential", "first-come"):
                 chunks = [RowChunk(o, x[o:o + size]) for o in range(0, x.shape[0], size)]
                 res = tsqr.stream_pass(chunks, sketch_rows=6, seed=11, combine_order=order)
                 key = f"{name}__c{size}__{order}"

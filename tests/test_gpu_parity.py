@@ -251,6 +251,20 @@ def test_sequential_and_first_come_orders(golden_tsqr):
         assert res.tree_depth == 0
 
 
+@pytest.mark.parametrize("size", [1, 7, 64])
+def test_first_come_single_thread_is_the_tree(golden_tsqr, size):
+    """reference tsqr.py:315-333: "first-come" with threads=1 runs the ordered tree branch and reports
+    reducer.depth (golden fixture generated by the live reference with combine_order="first-come")."""
+    x = golden_tsqr["tall_300x17__x"]
+    key = f"tall_300x17__c{size}__first-come"
+    for data in (dev, np.ascontiguousarray):
+        chunks = [tb.RowChunk(o, data(x[o:o + size])) for o in range(0, 300, size)]
+        res = tb.stream_pass(chunks, combine_order="first-come", threads=1, sketch_rows=6, seed=11)
+        assert rel_err(res.factor.entries, golden_tsqr[key + "__r"]) <= R_TOL
+        assert rel_err(res.sketch.entries, golden_tsqr[key + "__sketch"]) <= 1e-12
+        assert [res.rows, res.chunks, res.tree_depth] == list(golden_tsqr[key + "__meta"])
+
+
 def test_tree_result_deterministic():
     x = np.random.default_rng(4).uniform(0, 1, (50_000, 64))
     a = tb.factor_chunk(dev(x)).entries

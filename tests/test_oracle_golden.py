@@ -60,7 +60,7 @@ def test_reference_compiled_rng_if_built(golden_rng):
 
 @pytest.mark.parametrize("name", SMALL_CASES)
 @pytest.mark.parametrize("size", [1, 7, 64, None])
-@pytest.mark.parametrize("order", ["tree", "sequential"])
+@pytest.mark.parametrize("order", ["tree", "sequential", "first-come"])
 def test_stream_pass_matches_reference(golden_tsqr, oracle, name, size, order):
     x = golden_tsqr[f"{name}__x"]
     size = x.shape[0] if size is None else size
@@ -125,3 +125,45 @@ def test_config_rows_are_row_addressed(oracle):
         part = oracle.config_rows(spec, 100, 200, mix)
         assert np.array_equal(whole[100:300], part)
         assert (whole >= 0).all()
+
+
+def test_oracle_selection_matches_reference(golden_select, oracle):
+    """The oracle's SPA / XRAY / GP / NNLS restatement (select.py, nnls.py) reproduces the live
+    reference's selections and coefficients (tests/golden/select.npz)."""
+    for i in range(4):
+        rr = golden_select[f"m{i}"]
+        r = 4 if i < 2 else 8
+        assert oracle.spa(rr, r, golden_select[f"m{i}_l1"]) == list(golden_select[f"m{i}_spa"])
+        assert oracle.spa(rr, r) == list(golden_select[f"m{i}_spa_raw"])
+        kx = oracle.xray_order(rr, r)
+        assert kx == list(golden_select[f"m{i}_xray"])
+        h = oracle.compute_h(rr, kx)
+        np.testing.assert_allclose(h, golden_select[f"m{i}_h_xray"], atol=1e-12)
+        assert abs(oracle.relative_residual(rr, kx, h) - golden_select[f"m{i}_res_xray"][0]) <= 1e-12
+        gp, short = oracle.gp_select(golden_select[f"m{i}_sk"], r)
+        assert gp == list(golden_select[f"m{i}_gp"]) and short == golden_select[f"m{i}_gp_short"][0]
+    np.testing.assert_allclose(oracle.nnls_solve(golden_select["nnls_a"], golden_select["nnls_b"]),
+                               golden_select["nnls_y"], atol=1e-13)
+
+
+def test_oracle_c1_selection_matches_reference(golden_c1, oracle):
+    red = oracle.reduced_matrix(golden_c1["r"])
+    k_spa = oracle.spa(red, 20, golden_c1["l1"])
+    assert k_spa == list(golden_c1["k_spa"])
+    assert oracle.xray_order(red, 20) == list(golden_c1["k_xray"])
+    h = oracle.compute_h(red, k_spa)
+    np.testing.assert_allclose(h, golden_c1["h_spa"], atol=1e-10)
+    sk = golden_c1["sketch"] / golden_c1["l1"]
+    assert oracle.gp_select(sk, 20)[0] == list(golden_c1["k_gp"])
+
+
+def test_oracle_nnls_iteration_cap_keeps_best_iterate(oracle):
+    """nnls.py:96-103: hitting max_iter raises with the best iterate; best_effort keeps it."""
+    rng = np.random.default_rng(3)
+    a = rng.uniform(0, 1, (30, 6))
+    b = a @ np.array([1.0, 0, 2, 0, 0.5, 0]) - 0.1 * rng.uniform(0, 1, 30)
+    with pytest.raises(oracle.OracleNnlsIterationError) as e:
+        oracle.nnls_solve(a, b, max_iter=1)
+    assert e.value.best_y.shape == (6,) and (e.value.best_y >= 0).all()
+    full = oracle.nnls_solve(a, b)
+    assert (full >= 0).all()
