@@ -118,20 +118,20 @@ def test_config_reduced_rows_selection_matches_oracle(oracle, name, sigma, k):
     np.testing.assert_allclose(res.stats.l1, ref.l1, rtol=1e-12)
     if k:
         assert np.linalg.norm(res.sketch.entries - ref.sketch) <= 1e-12 * np.linalg.norm(ref.sketch)
+    # selection and coefficients: the device (best-iterate mode at the NNLS cap, tests/parity_full.py) vs the
+    # oracle's restatement of select.py / nnls.py on its own R, never skipped
+    from paper_1402_6964_b200.extremes import xray_order_device
+    from paper_1402_6964_b200.nonneg import solve_columns_device
+
     r = ospec.r
-    red_dev = tb.rsvd(res.factor)
-    red_ref = tb.rsvd(tb.TriangularFactor(r_ref))
-    stats_ref = tb.ColumnStats(np.array(ref.l1), np.sqrt(ref.sumsq))
-    k_dev = tb.spa(red_dev, r, normalize=True, stats=res.stats)
-    k_ref = tb.spa(red_ref, r, normalize=True, stats=stats_ref)
-    assert list(k_dev.indices) == list(k_ref.indices)
-    h_dev = tb.compute_h(red_dev, k_dev, device=True)
-    h_ref = tb.compute_h(red_ref, k_ref)
-    assert np.abs(h_dev.entries - h_ref.entries).max() <= H_TOL
-    kx_dev = tb.xray_greedy(red_dev, r, device=True)
-    try:
-        kx_ref = tb.xray_greedy(red_ref, r)
-    except tb.NumericalError:  # the host Lawson-Hanson can cycle at the tolerance
-        kx_ref = None
-    if kx_ref is not None:
-        assert list(kx_dev.indices) == list(kx_ref.indices)
+    m_dev = tb.rsvd(res.factor).reduced_matrix()
+    m_ref = oracle.reduced_matrix(r_ref)
+    k_dev = list(tb.spa(m_dev, r, normalize=True, stats=res.stats).indices)
+    k_ref = oracle.spa(m_ref, r, ref.l1)
+    assert k_dev == k_ref
+    h_dev = solve_columns_device(m_dev[:, k_dev], m_dev, capped=[])
+    h_ref, _ = oracle.compute_h(m_ref, k_ref, best_effort=True)
+    assert np.abs(h_dev - h_ref).max() <= H_TOL
+    kx_dev = xray_order_device(m_dev, r, capped=[])
+    kx_ref = oracle.xray_order(m_ref, r, best_effort=True)
+    assert kx_dev == kx_ref
