@@ -3,7 +3,7 @@ GB/s of X and % of roofline), one JSON line on rank 0.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--rows M]
   python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
-  python bench.py --impl reference            # the reference's CPU path (oracle port) on host cores
+  python bench.py --impl reference            # the reference's CPU path (baseline/_ref, else the oracle port)
 
 A step = one TSQR pass over the job's X (BASELINE config C2 by default: m = 2^26 rows, n = 200, fp64,
 107 GB resident in HBM; X row-sharded evenly over the N GPUs = config C3, strong scaling), i.e. the
@@ -15,6 +15,7 @@ under "gram" / "sketch".  X (107 GB) is far larger than L2 (126 MB), so no L2 fl
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import statistics
@@ -128,59 +129,117 @@ class ClockSampler:
 # reference arm / CPU baseline: the oracle port of the reference's stream_pass on host cores
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_available() -> bool:
+    """The unmodified reference package installed into baseline/_ref (tools/install_reference.sh)."""
+    return os.path.isfile(os.path.join(REF_DIR, "tsnmf", "tsqr.py"))
+
+
 def _cpu_worker(args):
+    """One host process: the reference's stream_pass over 8192-row RowChunks (two pre-generated chunks cycled:
+    the QR cost is data-independent).  impl "reference" = the installed reference package itself
+    (baseline/_ref, compiled backend, threads=1); "port" = the oracle's restatement of it."""
     import numpy as np
     from threadpoolctl import threadpool_limits
 
     from oracle import tsnmf_oracle as o
 
-    spec_name, n_chunks, chunk_rows, seed, sketch, start_at = args
+    spec_name, n_chunks, chunk_rows, seed, sketch, start_at, impl, threads = args
     spec = o.config_spec(spec_name)
     mix = o.config_mixing(spec)[0]
     bufs = [o.config_rows(spec, i * chunk_rows, chunk_rows, mix) for i in range(2)]
+    if impl == "reference":
+        sys.path.insert(0, REF_DIR)
+        import tsnmf
+
+        def run():
+            chunks = (tsnmf.RowChunk(row_offset=i * chunk_rows, data=bufs[i % 2]) for i in range(n_chunks))
+            res = tsnmf.stream_pass(chunks, sketch_rows=sketch, seed=seed, threads=threads)
+            return res.rows, np.asarray(res.factor.entries)
+    else:
+        def run():
+            res = o.stream_pass(((i * chunk_rows, bufs[i % 2]) for i in range(n_chunks)), sketch_rows=sketch,
+                                seed=seed)
+            return res.rows, np.asarray(res.r)
     while start_at and time.time() < start_at:  # all workers start the timed pass together
         time.sleep(0.001)
     with threadpool_limits(1):
         t0 = time.perf_counter()
-        res = o.stream_pass(((i * chunk_rows, bufs[i % 2]) for i in range(n_chunks)),
-                            sketch_rows=sketch, seed=seed)
+        rows, r = run()
         dt = time.perf_counter() - t0
-    return dt, res.rows, np.asarray(res.r)
+    return dt, rows, r
 
 
-def cpu_reference(spec_name: str, n: int, seconds: float, sketch=None):
-    """Time the reference algorithm (oracle port: per-8192-row-chunk LAPACK QR + TreeReducer,
-    reference tsqr.py:276-343) with one process per host core on a bounded sample; the per-process
-    factors are combined with the reference TreeReducer(combine) (SURVEY.md §8d best-effort CPU)."""
+def cpu_reference(spec_name: str, n: int, seconds: float, sketch=None, impl: str | None = None):
+    """Time the reference's CPU pass (per-8192-row-chunk LAPACK QR + TreeReducer, reference
+    tsqr.py:276-343) with one process per host core on a bounded sample; the per-process factors are
+    combined with the reference TreeReducer(combine) (SURVEY.md §8d best-effort CPU).  impl: "reference" (the
+    installed reference, default when present) or "port" (the oracle restatement)."""
     import multiprocessing as mpc
+
+    import numpy as np
 
     from oracle import tsnmf_oracle as o
 
+    impl = impl or ("reference" if reference_available() else "port")
     cores = len(os.sched_getaffinity(0))
     chunk_rows = 8192
     # calibrate: chunks on one core
-    probe = _cpu_worker((spec_name, 4, chunk_rows, 0, sketch, 0))[0] / 4
+    probe = _cpu_worker((spec_name, 4, chunk_rows, 0, sketch, 0, impl, 1))[0] / 4
     per_proc = max(2, int(seconds / max(probe, 1e-3)))
     ctx = mpc.get_context("fork")
     with ctx.Pool(cores) as pool:
-        outs = pool.map(_cpu_worker, [(spec_name, per_proc, chunk_rows, 0, sketch, time.time() + 3.0)] * cores)
+        outs = pool.map(_cpu_worker, [(spec_name, per_proc, chunk_rows, 0, sketch, time.time() + 3.0, impl, 1)]
+                        * cores)
     t0 = time.perf_counter()
-    red = o.TreeReducer(o.combine)
-    for _, _, r in outs:
-        red.push(r)
+    if impl == "reference":
+        sys.path.insert(0, REF_DIR)
+        import tsnmf
+
+        red = tsnmf.tsqr.TreeReducer(tsnmf.combine)
+        for _, _, r in outs:
+            red.push(tsnmf.TriangularFactor(entries=np.array(r)))
+    else:
+        red = o.TreeReducer(o.combine)
+        for _, _, r in outs:
+            red.push(r)
     red.result()
     wall = max(dt for dt, _, _ in outs) + (time.perf_counter() - t0)
     rows = sum(r for _, r, _ in outs)
     gbs = rows * n * 8 / wall / 1e9
-    return {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "port",
-            "sample": f"{rows} rows x {n} cols of {spec_name} ({cores} procs x {per_proc} chunks of {chunk_rows} "
-                      f"rows, numpy/OpenBLAS LAPACK QR per chunk + TreeReducer, 1 BLAS thread each; "
-                      f"time = slowest process + final combine)"
-                      + (f" + GX k={sketch}" if sketch else ""),
+    what = ("the installed reference package (baseline/_ref: tsnmf.stream_pass, compiled backend, threads=1) "
+            if impl == "reference" else "the oracle port of the reference's stream_pass ")
+    return {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "reference" if impl == "reference" else "port",
+            "sample": f"{rows} rows x {n} cols of {spec_name}: {cores} processes x {per_proc} chunks of "
+                      f"{chunk_rows} rows, each running {what}(numpy/OpenBLAS LAPACK QR per chunk, 1 BLAS "
+                      f"thread), factors combined by the reference TreeReducer(combine); time = slowest "
+                      f"process + final combine" + (f"; + GX k={sketch}" if sketch else ""),
             "seconds": wall}
 
 
+def as_shipped_reference(spec_name: str, n: int, seconds: float):
+    """The reference as a user runs it: ONE process, tsnmf.stream_pass(chunks, threads=<cores>) (its
+    thread-pool map, tsqr.py:247-273,315-333), 8192-row chunks, 1 BLAS thread."""
+    import multiprocessing as mpc
+
+    if not reference_available():
+        return None
+    cores = len(os.sched_getaffinity(0))
+    probe = _cpu_worker((spec_name, 4, 8192, 0, None, 0, "reference", 1))[0] / 4
+    n_chunks = max(8, int(seconds / max(probe, 1e-3)))
+    ctx = mpc.get_context("fork")
+    with ctx.Pool(1) as pool:
+        dt, rows, _ = pool.apply(_cpu_worker, ((spec_name, n_chunks, 8192, 0, None, 0, "reference", cores),))
+    return {"value": rows * n * 8 / dt / 1e9, "unit": "GB/s", "cores": cores, "kind": "reference",
+            "sample": f"{rows} rows x {n} cols of {spec_name}: one process, tsnmf.stream_pass(threads={cores}) "
+                      f"over 8192-row RowChunks (baseline/_ref, compiled backend, 1 BLAS thread)"}
+
+
 def run_reference(args):
+    """--impl reference: the reference's CPU path on the box's host cores (rank 0 only), best-effort form (one
+    process per core); the as-shipped single-process number is printed beside it."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -199,9 +258,15 @@ def run_reference(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": f"{args.config}: TSQR pass, m={spec.m}, n={spec.n} (bounded CPU sample)"},
-            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": base["cores"], "kind": "port",
+            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": base["cores"], "kind": base["kind"],
                              "sample": base["sample"]},
             "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    try:
+        shipped = as_shipped_reference(args.config, spec.n, max(4.0, args.cpu_seconds / 2))
+        if shipped:
+            line["as_shipped"] = shipped
+    except Exception as exc:
+        line["as_shipped"] = {"error": f"{type(exc).__name__}: {exc}"}
     print(json.dumps(line), flush=True)
 
 
@@ -252,6 +317,63 @@ def selection_timing(x, r, n):
         if hd is not None and hh is not None:
             sel["h_max_abs_diff"] = float(np.abs(hd - hh).max())
     return {k: v for k, v in sel.items() if v is not None}
+
+def e2e_legs(tb, x, n, devc):
+    """Two more end-to-end legs through the public API (world 1): (a) the reference's default chunking —
+    8192-row RowChunks from PAGEABLE host memory (matio.py:27; the host packs them into pinned staging);
+    (b) a file in the reference's binary format through ChunkReader(device=...) with and without the
+    reference's sha256 content hash (pipeline.py:157-159), the file already in the page cache."""
+    import numpy as np
+    import torch
+
+    out = {}
+    rows = min(int(x.shape[0]), 1 << 23)
+    pool_rows = min(rows, (2 << 30) // (8 * n))
+    pool = x[:pool_rows].cpu().numpy().copy()  # pageable
+
+    def chunks():
+        off = 0
+        while off < rows:
+            take = min(8192, rows - off)
+            src = off % pool_rows
+            take = min(take, pool_rows - src)
+            yield tb.RowChunk(off, pool[src:src + take])
+            off += take
+
+    tb.stream_pass(chunks())
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = tb.stream_pass(chunks())
+    dt = time.perf_counter() - t0
+    assert res.rows == rows
+    out["pageable_8192"] = {"value": rows * n * 8 / dt / 1e9, "unit": "GB/s", "rows": rows,
+                            "h2d_bytes_per_step": rows * n * 8, "d2h_bytes_per_step": (n * n + 2 * n) * 8,
+                            "api": "stream_pass over 8192-row RowChunks of pageable numpy memory"}
+    del pool
+    frows = min(int(x.shape[0]), 1 << 21)
+    fd, path = tempfile.mkstemp(suffix=".tsm")
+    os.close(fd)
+    try:
+        tb.write_matrix(path, x[:frows].cpu().numpy())
+        for label, hasher in (("file_device_reader", None), ("file_device_reader_sha256", "sha256")):
+            best = None
+            for _ in range(2):  # first read warms the page cache
+                h = hashlib.sha256() if hasher else None
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                res = tb.stream_pass(tb.ChunkReader(path, device=devc, hasher=h))
+                dt = time.perf_counter() - t0
+                best = dt if best is None else min(best, dt)
+            assert res.rows == frows
+            out[label] = {"value": frows * n * 8 / best / 1e9, "unit": "GB/s", "rows": frows,
+                          "api": "stream_pass(ChunkReader(path, device=cuda" + (", hasher=sha256" if hasher else "")
+                                 + ")), file in the page cache",
+                          "bound": "host sha256 of the byte stream (sequential by definition)" if hasher
+                                   else "page-cache read into pinned buffers"}
+    finally:
+        os.unlink(path)
+    return out
+
 
 def main():
     args = parse()
@@ -306,16 +428,20 @@ def main():
             sharded.exchange(part, dv.combine_factors)
         return r
 
+    # N > 1: the product's exchange (sharded.exchange: one all-gather of the packed partials + ordered sum)
     def gram_step():
         g, l1, sq = dv.gram(x, stats=True)
         if world > 1:
-            dist.all_reduce(g)
+            g = sharded.exchange(sharded.ShardPartials(r=None, l1=l1, sumsq=sq, rows=hi - lo, gram=g),
+                                 dv.combine_factors).gram
         return g
 
     def sketch_step():
         s = dv.sketch(x, lo, 0, args.k)
         if world > 1:
-            dist.all_reduce(s)
+            z = torch.zeros(n, dtype=torch.float64, device=devc)
+            s = sharded.exchange(sharded.ShardPartials(r=None, l1=z, sumsq=z, rows=hi - lo, sketch=s),
+                                 dv.combine_factors).sketch
         return s
 
     def timed(fn, steps, warmup, slot):
@@ -399,6 +525,18 @@ def main():
                         "kernel_ms": gk_ms, "kernel_tflops": gflops / (gk_ms * 1e-3) / 1e12,
                         "frac_fp64": gflops / (gk_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
                         "hbm_frac": bytes_local / (gk_ms * 1e-3) / 1e9 / hbm}
+        # size-independent full-m checks of this pass (parity against the oracle at full m is
+        # tests/parity_full.py -> profiles/r02_parity_full.json): R^T R = X^T X with X^T X from
+        # the independent Gram kernel, R upper triangular with a nonnegative diagonal
+        r_full = tsqr_step() if world == 1 else None
+        if r_full is not None:
+            g_full = gram_step()
+            rtr = r_full.T @ r_full
+            line["checks"] = {
+                "rtr_vs_gram_rel": float(torch.linalg.norm(rtr - g_full) / torch.linalg.norm(g_full)),
+                "r_strict_lower_zero": bool((torch.tril(r_full, -1) == 0).all()),
+                "r_diag_nonneg": bool((torch.diagonal(r_full) >= 0).all()),
+                "tolerance": "rtr_vs_gram_rel <= 1e-10"}
         sms, sk_ms, _, _ = timed(sketch_step, 2, 1, 3)
         sflops = 2.0 * args.k * n * (hi - lo)
         line["sketch"] = {"value": bytes_total / (sms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": sms,
@@ -456,6 +594,8 @@ def main():
                        "host_pool": f"{pool_rows} pinned rows cycled (QR cost is data-independent)",
                        "steps": e_steps, "timer": "host wall clock around the API call, barrier on both sides"}
         assert res.rows == hi - lo
+        if world == 1:
+            line["e2e_legs"] = e2e_legs(tb, x, n, devc)
 
     if rank == 0 and world == 1 and not args.no_cpu:
         try:

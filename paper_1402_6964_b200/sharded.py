@@ -42,25 +42,26 @@ class ShardPartials:
 
 def _pack(p: ShardPartials, n: int, k: int):
     t = dv.torch()
-    parts = [p.r.reshape(-1), p.l1.reshape(-1), p.sumsq.reshape(-1)]
+    parts = ([] if p.r is None else [p.r.reshape(-1)]) + [p.l1.reshape(-1), p.sumsq.reshape(-1)]
     if k:
         parts.append(p.sketch.reshape(-1))
     if p.gram is not None:
         parts.append(p.gram.reshape(-1))
-    parts.append(t.tensor([float(p.rows)], dtype=t.float64, device=p.r.device))
+    parts.append(t.tensor([float(p.rows)], dtype=t.float64, device=p.l1.device))
     return t.cat(parts)
 
 
 def exchange(p: ShardPartials, combine_stack, group=None) -> ShardPartials:
     """All-gather the packed partials and combine them deterministically.
 
-    combine_stack(rs: world x n x n) -> n x n factor, in TreeReducer order.
+    combine_stack(rs: world x n x n) -> n x n factor, in TreeReducer order.  ``p.r`` may be None (a Gram- or
+    sketch-only pass): then only the additive parts are exchanged.
     """
     import torch.distributed as dist
 
     t = dv.torch()
     world = dist.get_world_size(group)
-    n = int(p.r.shape[0])
+    n = int(p.l1.shape[0])
     k = int(p.sketch.shape[0]) if p.sketch is not None else 0
     flat = _pack(p, n, k)
     gathered = t.empty(world * flat.numel(), dtype=flat.dtype, device=flat.device)
@@ -74,7 +75,7 @@ def exchange(p: ShardPartials, combine_stack, group=None) -> ShardPartials:
         off += count
         return out
 
-    rs = take(n * n, (n, n))
+    rs = take(n * n, (n, n)) if p.r is not None else None
     l1s = take(n, (n,))
     sqs = take(n, (n,))
     sks = take(k * n, (k, n)) if k else None
@@ -87,7 +88,7 @@ def exchange(p: ShardPartials, combine_stack, group=None) -> ShardPartials:
             acc = acc + stack[i]
         return acc
 
-    r = combine_stack(rs.contiguous())
+    r = combine_stack(rs.contiguous()) if rs is not None else None
     return ShardPartials(r=r, l1=ordered_sum(l1s), sumsq=ordered_sum(sqs), rows=int(rows.sum().item()),
                          sketch=ordered_sum(sks) if sks is not None else None,
                          gram=ordered_sum(gs) if gs is not None else None)

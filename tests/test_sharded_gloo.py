@@ -110,8 +110,13 @@ def _worker_torch(rank, world, port, x, out_dir):
         part = sharded.ShardPartials(r=_torch_r(xs), l1=xs.abs().sum(0), sumsq=(xs * xs).sum(0), rows=hi - lo,
                                      gram=xs.T @ xs)
         out = sharded.exchange(part, _torch_combine_stack)
+        # Gram-only exchange (no factor packed; bench.py's Gram step at N > 1)
+        gonly = sharded.exchange(sharded.ShardPartials(r=None, l1=part.l1, sumsq=part.sumsq, rows=hi - lo,
+                                                       gram=part.gram), _torch_combine_stack)
+        assert gonly.r is None and gonly.rows == out.rows
         np.savez(os.path.join(out_dir, f"t{world}_rank{rank}.npz"), r=out.r.numpy(), l1=out.l1.numpy(),
-                 sq=out.sumsq.numpy(), g=out.gram.numpy(), rows=out.rows, has_sk=out.sketch is not None)
+                 sq=out.sumsq.numpy(), g=out.gram.numpy(), rows=out.rows, has_sk=out.sketch is not None,
+                 g_only=gonly.gram.numpy())
     finally:
         dist.destroy_process_group()
 
@@ -134,3 +139,4 @@ def test_exchange_product_packing_without_oracle(tmp_path, world, oracle):
     np.testing.assert_allclose(out["l1"], ref.l1, rtol=1e-13)
     np.testing.assert_allclose(out["sq"], ref.sumsq, rtol=1e-13)
     np.testing.assert_allclose(out["g"], x.T @ x, rtol=1e-12, atol=1e-12)
+    assert np.array_equal(out["g_only"], out["g"])

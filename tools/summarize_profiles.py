@@ -44,6 +44,10 @@ def full(rep, name, desc):
             lines.append(f"{k} = {d[k]} {u.get(k, '')}")
     open(os.path.join(out_dir, f"{tag}_{name}_ncu_full.txt"), "w").write("\n".join(lines) + "\n")
 
+if len(sys.argv) > 2 and sys.argv[2] == "--one":  # summarize_profiles.py TAG --one REP NAME DESC
+    full(sys.argv[3], sys.argv[4], sys.argv[5])
+    print(open(os.path.join(out_dir, f"{tag}_{sys.argv[4]}_ncu_full.txt")).read())
+    sys.exit(0)
 if os.path.exists(os.path.join(g, "launches.csv")):
     launches()
 for rep, name, desc in [("tsqr_leaf_full.ncu-rep", "tsqr_leaf", "tsqr_leaf_kernel on 2^21 x 200 (tools/run_kernel.py tsqr 2097152 200 1)"),
