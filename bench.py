@@ -30,6 +30,7 @@ sys.path.insert(0, ROOT)
 
 FP64_PEAK_TFLOPS = 37.0  # measured DMMA peak, profiles/r01_peaks.json (no FP64 entry in MEASURED_PEAKS.json)
 FP64_FMA_PEAK_TFLOPS = 34.2  # measured DFMA peak (same file): the narrow warp-leaf TSQR runs on the FMA pipe
+TSQR_N200_CAPTURE = "r01_tsqr_leaf_ncu_full.txt"  # ncu --set full of the n = 200 leaf, 2^21 rows
 METRIC = "1-pass TSQR/Gram GB/s of X and % of HBM peak at 1/2/4/8 B200 vs CPU ref"
 
 
@@ -482,10 +483,12 @@ def main():
     leaf_tf = leaf_flops / (leaf_ms * 1e-3) / 1e12
     plan = dv.tsqr_plan(n, hi - lo)
     narrow = plan["panel"] == 1  # n <= 32: register-block warp leaf (FP64 FMA), else the DMMA panel leaf
-    prof_file, prof_rows, prof_n = (("r01_tsqr_warp_leaf_ncu_full.txt", 1 << 22, 25) if narrow
-                                    else ("r01_tsqr_leaf_ncu_full.txt", 1 << 21, 200))
-    # the committed ncu capture is per width: traffic is only reported for the width it was taken at
-    tpr = ncu_traffic_per_row(os.path.join(ROOT, "profiles", prof_file), prof_rows) if n == prof_n else None
+    # the committed ncu captures are per width: traffic is only reported for a width one was taken at
+    captures = {25: ("r01_tsqr_warp_leaf_ncu_full.txt", 1 << 22), 64: ("r02_tsqr_leaf_n64_ncu_full.txt", 1 << 21),
+                200: (TSQR_N200_CAPTURE, 1 << 21)}
+    prof_file, prof_rows = captures.get(n, ("(none)", 0))
+    prof_n = n if n in captures else None
+    tpr = ncu_traffic_per_row(os.path.join(ROOT, "profiles", prof_file), prof_rows) if prof_n else None
     peak_tf = FP64_FMA_PEAK_TFLOPS if narrow else FP64_PEAK_TFLOPS
 
     line = {

@@ -124,8 +124,9 @@ __device__ __forceinline__ double fast_rcp(double a) {
   return y;
 }
 
+// bj0: shared-memory column of the panel (== j0 except in the split leaf, whose tiles live in slots)
 template <int RQ, bool kPreload>
-__device__ __forceinline__ void panel_factor_lazy(double* __restrict__ Bs, int lds, int brows, int j0,
+__device__ __forceinline__ void panel_factor_lazy(double* __restrict__ Bs, int lds, int brows, int j0, int bj0,
                                                   double* __restrict__ R, int npad, const double* __restrict__ Rd,
                                                   double* __restrict__ Tm, double* __restrict__ red, int lane,
                                                   int tq_p) {
@@ -134,7 +135,7 @@ __device__ __forceinline__ void panel_factor_lazy(double* __restrict__ Bs, int l
 #pragma unroll
   for (int q = 0; q < RQ; ++q) {
     const int rl = lane + 32 * q;
-    const double* rp = Bs + rl * lds + j0;
+    const double* rp = Bs + rl * lds + bj0;
 #pragma unroll
     for (int c = 0; c < kNB; c += 2) {
       double2 v = make_double2(0.0, 0.0);
@@ -261,7 +262,7 @@ __device__ __forceinline__ void panel_factor_lazy(double* __restrict__ Bs, int l
   for (int q = 0; q < RQ; ++q) {
     const int rl = lane + 32 * q;
     if (rl < brows) {
-      double* rp = Bs + rl * lds + j0;
+      double* rp = Bs + rl * lds + bj0;
 #pragma unroll
       for (int c = 0; c < kNB; c += 2) *reinterpret_cast<double2*>(rp + (c ^ sw)) = make_double2(x[q][c], x[q][c + 1]);
     }
@@ -295,10 +296,12 @@ __device__ __forceinline__ void stage_rdiag(double* __restrict__ dst, const doub
 //   W = R_p(:, cb) + V^T B(:, cb);  W' = T^T W;  R_p(:, cb) -= W';  B(:, cb) -= V W'.
 // One warp, no CTA barrier.  The R_p tiles are read from global memory (L2-resident R slot) at the start
 // so their latency hides behind the k-loop; R is updated in global memory.
+// (vj, pcbs: shared-memory columns of V and of the tiles; j0, cbs: logical, for R)
 template <int G>
-__device__ __forceinline__ void update_cbs(double* __restrict__ Bs, int lds, int brows, int j0,
+__device__ __forceinline__ void update_cbs(double* __restrict__ Bs, int lds, int brows, int j0, int vj,
                                            double* __restrict__ R, int npad, const double* __restrict__ Tm,
-                                           double* __restrict__ Wsc, const int (&cbs)[G], int lane, int tq_p) {
+                                           double* __restrict__ Wsc, const int (&cbs)[G], const int (&pcbs)[G],
+                                           int lane, int tq_p) {
   const int frag_col = (lane >> 2) ^ ((lane & 2) << 1);  // slab fragment: row i + l%4, col l/4
   const int vsw = ((lane >> 2) & 2) << 1;                // V / C-tile rows 8rb + l/4
   double acc0[G][2], acc1[G][2], rinit[G][2];
@@ -317,11 +320,11 @@ __device__ __forceinline__ void update_cbs(double* __restrict__ Bs, int lds, int
   for (int i = 0; i < brows; i += 8) {
     const double* r0 = slab + i * lds;
     const double* r1 = r0 + 4 * lds;
-    const double a0 = r0[j0], a1 = r1[j0];
+    const double a0 = r0[vj], a1 = r1[vj];
 #pragma unroll
     for (int gg = 0; gg < G; ++gg) {
-      dmma(acc0[gg][0], acc0[gg][1], a0, r0[8 * cbs[gg]]);
-      dmma(acc1[gg][0], acc1[gg][1], a1, r1[8 * cbs[gg]]);
+      dmma(acc0[gg][0], acc0[gg][1], a0, r0[pcbs[gg]]);
+      dmma(acc1[gg][0], acc1[gg][1], a1, r1[pcbs[gg]]);
     }
   }
   TQ_TRACE(21);
@@ -352,13 +355,13 @@ __device__ __forceinline__ void update_cbs(double* __restrict__ Bs, int lds, int
   for (int rb = 0; rb < brows / 8; rb += 2) {
     double* rowa = Bs + (8 * rb + (lane >> 2)) * lds;
     double* rowb = rowa + 8 * lds;
-    const double a0 = rowa[j0 + ((lane & 3) ^ vsw)], a1 = rowa[j0 + ((4 + (lane & 3)) ^ vsw)];
-    const double b0 = rowb[j0 + ((lane & 3) ^ vsw)], b1 = rowb[j0 + ((4 + (lane & 3)) ^ vsw)];
+    const double a0 = rowa[vj + ((lane & 3) ^ vsw)], a1 = rowa[vj + ((4 + (lane & 3)) ^ vsw)];
+    const double b0 = rowb[vj + ((lane & 3) ^ vsw)], b1 = rowb[vj + ((4 + (lane & 3)) ^ vsw)];
     double2 ca[G], cb2[G];
 #pragma unroll
     for (int gg = 0; gg < G; ++gg) {
-      ca[gg] = *reinterpret_cast<const double2*>(rowa + 8 * cbs[gg] + ((2 * (lane & 3)) ^ vsw));
-      cb2[gg] = *reinterpret_cast<const double2*>(rowb + 8 * cbs[gg] + ((2 * (lane & 3)) ^ vsw));
+      ca[gg] = *reinterpret_cast<const double2*>(rowa + pcbs[gg] + ((2 * (lane & 3)) ^ vsw));
+      cb2[gg] = *reinterpret_cast<const double2*>(rowb + pcbs[gg] + ((2 * (lane & 3)) ^ vsw));
     }
 #pragma unroll
     for (int gg = 0; gg < G; ++gg) {
@@ -372,8 +375,8 @@ __device__ __forceinline__ void update_cbs(double* __restrict__ Bs, int lds, int
     }
 #pragma unroll
     for (int gg = 0; gg < G; ++gg) {
-      *reinterpret_cast<double2*>(rowa + 8 * cbs[gg] + ((2 * (lane & 3)) ^ vsw)) = ca[gg];
-      *reinterpret_cast<double2*>(rowb + 8 * cbs[gg] + ((2 * (lane & 3)) ^ vsw)) = cb2[gg];
+      *reinterpret_cast<double2*>(rowa + pcbs[gg] + ((2 * (lane & 3)) ^ vsw)) = ca[gg];
+      *reinterpret_cast<double2*>(rowb + pcbs[gg] + ((2 * (lane & 3)) ^ vsw)) = cb2[gg];
     }
   }
   TQ_TRACE(23);
@@ -460,10 +463,10 @@ __device__ __forceinline__ void lookahead_single(double* __restrict__ Bs, int ld
 // tile), the two partial W tiles meet through shared memory (one 64-thread barrier), both warps form the
 // same W' = T^T W (fixed summation order), the helper writes R_p -= W', and each warp updates its half of
 // the row blocks of B -= V W'.  Two dependency chains interleave on the SMSP's tensor pipe.
-__device__ __forceinline__ void lookahead_pair(double* __restrict__ Bs, int lds, int brows, int j0,
+__device__ __forceinline__ void lookahead_pair(double* __restrict__ Bs, int lds, int brows, int j0, int vj,
                                                double* __restrict__ R, int npad, const double* __restrict__ Tm,
-                                               double* __restrict__ Wpart, double* __restrict__ Wsc, int cb, int h,
-                                               int lane) {
+                                               double* __restrict__ Wpart, double* __restrict__ Wsc, int cb, int pcb,
+                                               int h, int lane) {
   const int frag_col = (lane >> 2) ^ ((lane & 2) << 1);
   const int vsw = ((lane >> 2) & 2) << 1;
   double* rtile = R + (int64_t)(j0 + (lane >> 2)) * npad + 8 * cb + 2 * (lane & 3);
@@ -481,15 +484,15 @@ __device__ __forceinline__ void lookahead_pair(double* __restrict__ Bs, int lds,
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const double* r = slab + (i + 4 * u) * lds;
-      a[u] = r[j0];
-      b[u] = r[8 * cb];
+      a[u] = r[vj];
+      b[u] = r[pcb];
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) dmma(c[u][0], c[u][1], a[u], b[u]);
   }
   for (; i < i_end; i += 4) {
     const double* r = slab + i * lds;
-    dmma(c[0][0], c[0][1], r[j0], r[8 * cb]);
+    dmma(c[0][0], c[0][1], r[vj], r[pcb]);
   }
   const int ci = (lane >> 2) * 8 + 2 * (lane & 3);
   Wpart[h * 64 + ci] = ((c[0][0] + c[1][0]) + (c[2][0] + c[3][0])) + rinit.x;
@@ -522,23 +525,23 @@ __device__ __forceinline__ void lookahead_pair(double* __restrict__ Bs, int lds,
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       rows[u] = Bs + (8 * (rb + u) + (lane >> 2)) * lds;
-      va[u] = rows[u][j0 + ((lane & 3) ^ vsw)];
-      vb[u] = rows[u][j0 + ((4 + (lane & 3)) ^ vsw)];
-      cv[u] = *reinterpret_cast<const double2*>(rows[u] + 8 * cb + ((2 * (lane & 3)) ^ vsw));
+      va[u] = rows[u][vj + ((lane & 3) ^ vsw)];
+      vb[u] = rows[u][vj + ((4 + (lane & 3)) ^ vsw)];
+      cv[u] = *reinterpret_cast<const double2*>(rows[u] + pcb + ((2 * (lane & 3)) ^ vsw));
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) dmma(cv[u].x, cv[u].y, va[u], wb0);
 #pragma unroll
     for (int u = 0; u < 4; ++u) dmma(cv[u].x, cv[u].y, vb[u], wb1);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) *reinterpret_cast<double2*>(rows[u] + 8 * cb + ((2 * (lane & 3)) ^ vsw)) = cv[u];
+    for (int u = 0; u < 4; ++u) *reinterpret_cast<double2*>(rows[u] + pcb + ((2 * (lane & 3)) ^ vsw)) = cv[u];
   }
   for (; rb < rb_end; ++rb) {
     double* row = Bs + (8 * rb + (lane >> 2)) * lds;
-    double2 cv = *reinterpret_cast<const double2*>(row + 8 * cb + ((2 * (lane & 3)) ^ vsw));
-    dmma(cv.x, cv.y, row[j0 + ((lane & 3) ^ vsw)], wb0);
-    dmma(cv.x, cv.y, row[j0 + ((4 + (lane & 3)) ^ vsw)], wb1);
-    *reinterpret_cast<double2*>(row + 8 * cb + ((2 * (lane & 3)) ^ vsw)) = cv;
+    double2 cv = *reinterpret_cast<const double2*>(row + pcb + ((2 * (lane & 3)) ^ vsw));
+    dmma(cv.x, cv.y, row[vj + ((lane & 3) ^ vsw)], wb0);
+    dmma(cv.x, cv.y, row[vj + ((4 + (lane & 3)) ^ vsw)], wb1);
+    *reinterpret_cast<double2*>(row + pcb + ((2 * (lane & 3)) ^ vsw)) = cv;
   }
 }
 
@@ -647,12 +650,12 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
         if (p > p0) named_sync(kBarColsReady, kThr);
         TQ_RESOLVE(Rdg);
         TQ_TRACE(1);
-        panel_factor_lazy<RQ, kPreload>(Bs, lds, brows, j0, R, npad, Rdc, Tm + buf * kNB * kNB, red, lane, tq_p);
+        panel_factor_lazy<RQ, kPreload>(Bs, lds, brows, j0, j0, R, npad, Rdc, Tm + buf * kNB * kNB, red, lane, tq_p);
         TQ_TRACE(2);
         named_arrive(kBarPanelDone, kThr);
         if (kPairLookahead && more) {
           __syncwarp();  // the warp's own V / T stores are visible to all its lanes
-          lookahead_pair(Bs, lds, brows, j0, R, npad, Tmc, Wpart, Wsc, p + 1, 0, lane);
+          lookahead_pair(Bs, lds, brows, j0, j0, R, npad, Tmc, Wpart, Wsc, p + 1, 8 * (p + 1), 0, lane);
         }
       } else if (warp == kHelper) {
         // helper on SMSP 0: the lookahead starts the moment the panel is published (not after the GEMM
@@ -664,7 +667,7 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
           stage_rdiag(Rdg + (buf ^ 1) * kNB * kNB, R, npad, j0 + kNB, lane);
           cp_async_commit();
           if (kPairLookahead)
-            lookahead_pair(Bs, lds, brows, j0, R, npad, Tmc, Wpart, Wsc, p + 1, 1, lane);
+            lookahead_pair(Bs, lds, brows, j0, j0, R, npad, Tmc, Wpart, Wsc, p + 1, 8 * (p + 1), 1, lane);
           else
             lookahead_single(Bs, lds, brows, j0, R, npad, Tmc, Wsc, p + 1, lane);
           cp_async_wait<0>();
@@ -688,16 +691,20 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
           }
           // a short last group is updated in one call (shared V fragment loads), not block by block
           if (cnt_g == G) {
-            update_cbs<G>(Bs, lds, brows, j0, R, npad, Tmc, Wsc, cbs, lane, tq_p);
+            const int pc[G] = {8 * cbs[0], 8 * cbs[1], 8 * cbs[2], 8 * cbs[3]};
+            update_cbs<G>(Bs, lds, brows, j0, j0, R, npad, Tmc, Wsc, cbs, pc, lane, tq_p);
           } else if (cnt_g == 3) {
             const int three[3] = {cbs[0], cbs[1], cbs[2]};
-            update_cbs<3>(Bs, lds, brows, j0, R, npad, Tmc, Wsc, three, lane, tq_p);
+            const int pc[3] = {8 * cbs[0], 8 * cbs[1], 8 * cbs[2]};
+            update_cbs<3>(Bs, lds, brows, j0, j0, R, npad, Tmc, Wsc, three, pc, lane, tq_p);
           } else if (cnt_g == 2) {
             const int two[2] = {cbs[0], cbs[1]};
-            update_cbs<2>(Bs, lds, brows, j0, R, npad, Tmc, Wsc, two, lane, tq_p);
+            const int pc[2] = {8 * cbs[0], 8 * cbs[1]};
+            update_cbs<2>(Bs, lds, brows, j0, j0, R, npad, Tmc, Wsc, two, pc, lane, tq_p);
           } else if (cnt_g == 1) {
             const int one[1] = {cbs[0]};
-            update_cbs<1>(Bs, lds, brows, j0, R, npad, Tmc, Wsc, one, lane, tq_p);
+            const int pc[1] = {8 * cbs[0]};
+            update_cbs<1>(Bs, lds, brows, j0, j0, R, npad, Tmc, Wsc, one, pc, lane, tq_p);
           }
         }
       }
@@ -749,6 +756,296 @@ __global__ void __launch_bounds__(32 * tq_warps<MINB>(), MINB)
   }
   tsqr_fold<RQ, MINB != 2, tq_warps<MINB>()>(slots + dst * ss, slots + srcs * ss, g.npad, g.npad, g.npad, g, true, false,
                                               nullptr, smem);
+}
+
+// ---------------------------------------------------------------------------
+// Split leaf (wide n, e.g. config C2 n = 200): 256-row blocks, twice the rows in flight of the 128-row
+// leaf above.  Throughput of the fold is (rows in flight) / (n x per-column panel latency) and the
+// 227 KB of shared memory hold only 128 rows x 200 columns, so the block is split by columns: the left
+// S = ceil(npanels / 2) column tiles (8 columns each) live in shared memory, the right ones in a per-leaf
+// L2-resident workspace (brows x 8(npanels - S) doubles).  Tiles are updated where they live (the GEMM
+// warps' trailing update of a workspace tile streams it through registers, DMMA operands from the
+// shared-memory V), and they move in as the left tiles die: right-looking QR frees tile s once panel s's
+// trailing update is done, so in iteration p = t - S + 1 the update of right tile t (by panel p) reads
+// the workspace and writes shared slot t - S.  Panel p and the lookahead tile p + 1 are therefore always
+// in shared memory (S >= 3).  Logical tile t lives in slot t (t < S) or t - S (t >= S, migrated);
+// R is addressed logically.  The first update of a right tile reads X directly (zero-filling rows past
+// the end and padding columns) and accumulates its column l1 / sum of squares on the way.
+constexpr int kSplitRows = 256;
+constexpr int kSplitRq = kSplitRows / 32;
+
+struct SplitGeom {
+  int n, npad;  // data / padded columns
+  int S;        // shared-memory tile slots (left tiles 0..S-1)
+  int lds;      // shared row stride (8 S rounded to % 16 == 8)
+  int wld;      // workspace row stride (8 (npanels - S))
+};
+
+__host__ __device__ inline TqGeom split_tq_geom(const SplitGeom& sg) {
+  TqGeom g;
+  g.n = sg.n;
+  g.npad = sg.npad;
+  g.lds = sg.lds;
+  g.brows = kSplitRows;
+  return g;
+}
+
+// One right tile (logical column block cb) updated with panel (j0)'s block reflector, data streamed from
+// global memory (X when kFromX, else the workspace) and written to the workspace (or, kToSmem, to the
+// swizzled shared slot at column dcol).  Lane l holds the tile in the DMMA B-operand layout (row 4s + l%4,
+// col l/4 in register s) for W = R_p + V^T B; the C-tile layout of B -= V W' (row l/4, cols 2(l%4)..+1)
+// is gathered from those registers by shuffles, so the tile is read from L2 once.
+template <bool kFromX, bool kToSmem>
+__device__ __forceinline__ void update_global(const double* __restrict__ Bs, int lds, int vj, int j0,
+                                              const double* __restrict__ src, int64_t lsrc, int vrows, int vcols,
+                                              double* __restrict__ dst, int64_t ldst, double* __restrict__ Bd,
+                                              int dcol, double* __restrict__ R, int npad, int cb,
+                                              const double* __restrict__ Tm, double* __restrict__ Wsc, int lane,
+                                              double& sa, double& sq) {
+  constexpr int K = kSplitRows / 4;  // k-steps (registers per lane)
+  const int frag_col = (lane >> 2) ^ ((lane & 2) << 1);
+  const int vsw = ((lane >> 2) & 2) << 1;
+  double* rtile = R + (int64_t)(j0 + (lane >> 2)) * npad + 8 * cb + 2 * (lane & 3);
+  const double2 rinit = *reinterpret_cast<const double2*>(rtile);
+  double b[K];
+  {
+    const double* bp = src + (int64_t)(lane & 3) * lsrc + (lane >> 2);
+    const bool colok = !kFromX || (lane >> 2) < vcols;
+#pragma unroll
+    for (int s = 0; s < K; ++s) {
+      const int row = 4 * s + (lane & 3);
+      if (kFromX)
+        b[s] = (colok && row < vrows) ? __ldcs(bp + (int64_t)4 * s * lsrc) : 0.0;
+      else
+        b[s] = __ldcg(bp + (int64_t)4 * s * lsrc);
+    }
+  }
+  double c[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+  const double* vslab = Bs + (lane & 3) * lds + frag_col + vj;
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+    dmma(c[s & 3][0], c[s & 3][1], vslab[4 * s * lds], b[s]);
+    if (kFromX) {
+      sa += fabs(b[s]);
+      sq = fma(b[s], b[s], sq);
+    }
+  }
+  const int ci = (lane >> 2) * 8 + 2 * (lane & 3);
+  Wsc[ci] = ((c[0][0] + c[1][0]) + (c[2][0] + c[3][0])) + rinit.x;
+  Wsc[ci + 1] = ((c[0][1] + c[1][1]) + (c[2][1] + c[3][1])) + rinit.y;
+  __syncwarp();
+  double w0 = 0.0, w1 = 0.0;
+#pragma unroll
+  for (int k0 = 0; k0 < 8; k0 += 4)
+    dmma(w0, w1, Tm[(k0 + (lane & 3)) * kNB + (lane >> 2)], Wsc[(k0 + (lane & 3)) * 8 + (lane >> 2)]);
+  *reinterpret_cast<double2*>(rtile) = make_double2(rinit.x - w0, rinit.y - w1);
+  __syncwarp();
+  Wsc[ci] = w0;
+  Wsc[ci + 1] = w1;
+  __syncwarp();
+  const double wb0 = -Wsc[(lane & 3) * 8 + (lane >> 2)];
+  const double wb1 = -Wsc[(4 + (lane & 3)) * 8 + (lane >> 2)];
+  __syncwarp();
+  // C tile of row block rb: element (8 rb + l/4, c) is register 2 rb + (l >> 4) of lane 4 c + (l/4) % 4
+  const int src0 = 8 * (lane & 3) + ((lane >> 2) & 3);
+  const bool hi = (lane >> 4) != 0;
+#pragma unroll
+  for (int rb = 0; rb < kSplitRows / 8; ++rb) {
+    const double x0a = __shfl_sync(0xffffffffu, b[2 * rb], src0);
+    const double x0b = __shfl_sync(0xffffffffu, b[2 * rb + 1], src0);
+    const double x1a = __shfl_sync(0xffffffffu, b[2 * rb], src0 + 4);
+    const double x1b = __shfl_sync(0xffffffffu, b[2 * rb + 1], src0 + 4);
+    double cx = hi ? x0b : x0a, cy = hi ? x1b : x1a;
+    const int row = 8 * rb + (lane >> 2);
+    const double* vrow = Bs + row * lds + vj;
+    dmma(cx, cy, vrow[(lane & 3) ^ vsw], wb0);
+    dmma(cx, cy, vrow[(4 + (lane & 3)) ^ vsw], wb1);
+    if (kToSmem)
+      *reinterpret_cast<double2*>(Bd + row * lds + dcol + ((2 * (lane & 3)) ^ vsw)) = make_double2(cx, cy);
+    else
+      __stcg(reinterpret_cast<double2*>(dst + (int64_t)row * ldst + 2 * (lane & 3)), make_double2(cx, cy));
+  }
+}
+
+template <int RQ>
+__device__ void tsqr_split_fold(double* __restrict__ R, const double* __restrict__ X, int64_t nrows, int64_t ldx,
+                                int ncols, const SplitGeom sg, double* __restrict__ ws,
+                                double* __restrict__ stats_out, double* smem) {
+  using L = TqLayout;
+  constexpr int G = 4;
+  constexpr int W = kTqWarps;
+  constexpr int kThr = 32 * W;
+  constexpr int kHelper = 4;
+  constexpr int kGemm = W - 2;
+  const TqGeom g = split_tq_geom(sg);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int npad = g.npad, lds = g.lds, brows = g.brows;
+  const int S = sg.S, npanels = npad / kNB;
+  const int lcols = 8 * S;  // logical columns staged into shared memory
+  double* Bs = smem;
+  double* Rdg = smem + L::rd(g);
+  double* Tm = smem + L::tm(g);
+  double* red = smem + L::red(g);
+  double* Wsc = smem + L::wsc(g) + warp * kNB * 8;
+  double* Wpart = smem + L::wpart(g);
+  const bool vec16 = ((ldx & 1) == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
+  const int scols = ncols < lcols ? ncols : lcols;
+  auto slot_col = [&](int t) { return 8 * (t < S ? t : t - S); };
+
+  for (int64_t idx = tid; idx < (int64_t)npad * npad; idx += kThr) R[idx] = 0.0;
+  constexpr int kSH = (512 + kThr - 1) / kThr;
+  double l1a[kSH], sqa[kSH];
+#pragma unroll
+  for (int h = 0; h < kSH; ++h) l1a[h] = sqa[h] = 0.0;
+  // right-tile stats: the GEMM warp that updates right tile t in iteration 0 (t = 2 + gi + kGemm * gg)
+  double rsa[G], rsq[G];
+#pragma unroll
+  for (int gg = 0; gg < G; ++gg) rsa[gg] = rsq[gg] = 0.0;
+  const int gi = warp == 0 || warp == kHelper ? -1 : gemm_index(warp);
+
+  for (int64_t r0 = 0; r0 < nrows; r0 += brows) {
+    const int cnt = (int)min64(brows, nrows - r0);
+    const double* xb = X + r0 * ldx;
+    __syncthreads();
+    stage_block(Bs, lds, xb, ldx, cnt, scols, brows, lcols, vec16);
+    if (warp == 0) stage_rdiag(Rdg, R, npad, 0, lane);
+    cp_async_commit();
+    // the next block's right columns into L2 (its first trailing update reads X)
+    if (r0 + brows < nrows && ncols > lcols) {
+      const int64_t nrow0 = r0 + brows;
+      const int nr = (int)min64(brows, nrows - nrow0);
+      for (int r = tid; r < nr; r += kThr) {
+        const char* a = reinterpret_cast<const char*>(X + (nrow0 + r) * ldx + lcols);
+        const char* e = reinterpret_cast<const char*>(X + (nrow0 + r) * ldx + ncols);
+        for (const char* q = (const char*)((uintptr_t)a & ~(uintptr_t)127); q < e; q += 128)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+      }
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    if (stats_out) {
+#pragma unroll
+      for (int h = 0; h < kSH; ++h) {
+        const int col = tid + h * kThr;
+        if (col < scols) {
+          double a = l1a[h], q = sqa[h];
+          for (int i = 0; i < cnt; ++i) {
+            const double v = Bs[i * lds + (col ^ swz(i))];
+            a += fabs(v);
+            q = fma(v, v, q);
+          }
+          l1a[h] = a;
+          sqa[h] = q;
+        }
+      }
+    }
+    for (int p = 0; p < npanels; ++p) {
+      const int j0 = p * kNB;
+      const int vj = slot_col(p);
+      const int buf = p & 1;
+      const double* Rdc = Rdg + buf * kNB * kNB;
+      const double* Tmc = Tm + buf * kNB * kNB;
+      const bool more = p + 1 < npanels;
+      const int tq_p = -1;
+      if (warp == 0) {
+        if (p > 0) named_sync(kBarColsReady, kThr);
+        panel_factor_lazy<RQ, true>(Bs, lds, brows, j0, vj, R, npad, Rdc, Tm + buf * kNB * kNB, red, lane, tq_p);
+        named_arrive(kBarPanelDone, kThr);
+        if (more) {
+          __syncwarp();
+          lookahead_pair(Bs, lds, brows, j0, vj, R, npad, Tmc, Wpart, Wsc, p + 1, slot_col(p + 1), 0, lane);
+        }
+      } else if (warp == kHelper) {
+        named_sync(kBarPanelDone, kThr);
+        if (more) {
+          stage_rdiag(Rdg + (buf ^ 1) * kNB * kNB, R, npad, j0 + kNB, lane);
+          cp_async_commit();
+          lookahead_pair(Bs, lds, brows, j0, vj, R, npad, Tmc, Wpart, Wsc, p + 1, slot_col(p + 1), 1, lane);
+          cp_async_wait<0>();
+          __syncwarp();
+          named_arrive(kBarColsReady, kThr);
+        }
+      } else {
+        named_sync(kBarPanelDone, kThr);
+        if (more) named_arrive(kBarColsReady, kThr);
+        for (int base = p + 2 + gi; base < npanels; base += kGemm * G) {
+          // shared tiles of this group in one call (shared V fragment loads); workspace tiles one by one.
+          // Tiles in shared memory are those below S + max(p - 1, 0): a prefix of the group.
+          const int lim = min(npanels, S + (p > 0 ? p - 1 : 0));
+          const int c4[4] = {base, base + kGemm, base + 2 * kGemm, base + 3 * kGemm};
+          const int ns = c4[3] < lim ? 4 : (c4[2] < lim ? 3 : (c4[1] < lim ? 2 : (c4[0] < lim ? 1 : 0)));
+          if (ns == 4) {
+            const int p4[4] = {slot_col(c4[0]), slot_col(c4[1]), slot_col(c4[2]), slot_col(c4[3])};
+            update_cbs<4>(Bs, lds, brows, j0, vj, R, npad, Tmc, Wsc, c4, p4, lane, tq_p);
+          } else if (ns == 3) {
+            const int c3[3] = {c4[0], c4[1], c4[2]}, p3[3] = {slot_col(c4[0]), slot_col(c4[1]), slot_col(c4[2])};
+            update_cbs<3>(Bs, lds, brows, j0, vj, R, npad, Tmc, Wsc, c3, p3, lane, tq_p);
+          } else if (ns == 2) {
+            const int c2[2] = {c4[0], c4[1]}, p2[2] = {slot_col(c4[0]), slot_col(c4[1])};
+            update_cbs<2>(Bs, lds, brows, j0, vj, R, npad, Tmc, Wsc, c2, p2, lane, tq_p);
+          } else if (ns == 1) {
+            const int c1[1] = {c4[0]}, p1[1] = {slot_col(c4[0])};
+            update_cbs<1>(Bs, lds, brows, j0, vj, R, npad, Tmc, Wsc, c1, p1, lane, tq_p);
+          }
+#pragma unroll
+          for (int gg = 0; gg < G; ++gg) {
+            const int t = base + kGemm * gg;
+            if (t >= npanels || t < lim) continue;
+            double* wt = ws + 8 * (t - S);
+            if (p == 0) {
+              update_global<true, false>(Bs, lds, vj, j0, xb + 8 * t, ldx, cnt, ncols - 8 * t, wt, sg.wld, nullptr,
+                                         0, R, npad, t, Tmc, Wsc, lane, rsa[gg], rsq[gg]);
+            } else if (t - S + 1 == p) {
+              double d0 = 0.0, d1 = 0.0;
+              update_global<false, true>(Bs, lds, vj, j0, wt, sg.wld, brows, 8, nullptr, 0, Bs, 8 * (t - S), R,
+                                         npad, t, Tmc, Wsc, lane, d0, d1);
+            } else {
+              double d0 = 0.0, d1 = 0.0;
+              update_global<false, false>(Bs, lds, vj, j0, wt, sg.wld, brows, 8, wt, sg.wld, nullptr, 0, R, npad,
+                                          t, Tmc, Wsc, lane, d0, d1);
+            }
+          }
+        }
+      }
+    }
+  }
+  if (stats_out) {
+#pragma unroll
+    for (int h = 0; h < kSH; ++h) {
+      const int col = tid + h * kThr;
+      if (col < lcols) {
+        stats_out[col] = l1a[h];
+        stats_out[npad + col] = sqa[h];
+      }
+    }
+    if (gi >= 0) {
+#pragma unroll
+      for (int gg = 0; gg < G; ++gg) {
+        double a = rsa[gg], q = rsq[gg];
+        a += __shfl_xor_sync(0xffffffffu, a, 1);
+        q += __shfl_xor_sync(0xffffffffu, q, 1);
+        a += __shfl_xor_sync(0xffffffffu, a, 2);
+        q += __shfl_xor_sync(0xffffffffu, q, 2);
+        const int t = 2 + gi + kGemm * gg;
+        if (t >= S && t < npanels && (lane & 3) == 0) {
+          stats_out[8 * t + (lane >> 2)] = a;
+          stats_out[npad + 8 * t + (lane >> 2)] = q;
+        }
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256, 1)
+    tsqr_split_leaf_kernel(const double* __restrict__ x, int64_t m, int64_t ldx, int64_t rows_per_cta, SplitGeom sg,
+                           double* __restrict__ slots, double* __restrict__ stats, double* __restrict__ wsr) {
+  extern __shared__ __align__(16) double smem[];
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t cnt = max64(0, min64(rows_per_cta, m - r0));
+  double* R = slots + (int64_t)blockIdx.x * sg.npad * sg.npad;
+  double* st = stats ? stats + (int64_t)blockIdx.x * 2 * sg.npad : nullptr;
+  double* ws = wsr + (int64_t)blockIdx.x * kSplitRows * sg.wld;
+  tsqr_split_fold<kSplitRq>(R, x + r0 * ldx, cnt, ldx, sg.n, sg, ws, st, smem);
 }
 
 // ---------------------------------------------------------------------------
@@ -1489,6 +1786,49 @@ int small_leaf(const double* x, int64_t m, int n, int64_t ldx, int64_t rpw, int 
   }
 }
 
+// Split leaf (256-row blocks, right column tiles in an L2 workspace): 105 <= n <= 208 (14..26 panels, so
+// the shared half holds <= 13 tiles); TSNMF_TSQR_SPLIT=0 selects the 128/160-row leaf.
+bool split_path(int n) {
+  if (n < 105 || n > 208) return false;
+  if (const char* e = getenv("TSNMF_TSQR_SPLIT")) return atoi(e) != 0;
+  return true;
+}
+SplitGeom split_geom(int n) {
+  SplitGeom sg;
+  sg.n = n;
+  sg.npad = (int)round_up(n, kNB);
+  const int np = sg.npad / kNB;
+  sg.S = (np + 1) / 2;
+  sg.lds = smem_stride(8 * sg.S);
+  sg.wld = 8 * (np - sg.S);
+  return sg;
+}
+size_t split_smem(const SplitGeom& sg) { return TqLayout::bytes(split_tq_geom(sg)); }
+void split_plan(int n, int64_t m, int* nleaves, int64_t* rows_per_cta) {
+  const int64_t npad = round_up(n, kNB);
+  const int64_t max_leaves = device_sms();
+  const int64_t min_rows = max64(kSplitRows, 2 * npad);
+  int64_t leaves = max64(1, min64(max_leaves, ceil_div(m, min_rows)));
+  int64_t rpc = round_up(ceil_div(m, leaves), kSplitRows);
+  *nleaves = (int)ceil_div(m, rpc);
+  *rows_per_cta = rpc;
+}
+size_t split_ws_doubles(const SplitGeom& sg, int nleaves) { return (size_t)nleaves * kSplitRows * sg.wld; }
+int split_leaf(const double* x, int64_t m, int64_t ldx, const SplitGeom& sg, int nleaves, int64_t rpc,
+               double* slots, double* stats, double* wsr, cudaStream_t st) {
+  static PerDeviceFlag attr;
+  const size_t smem = split_smem(sg);
+  if (!attr.is_set()) {
+    TSNMF_CUDA_CHECK(cudaFuncSetAttribute(tsqr_split_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+    attr.set();
+  }
+  prof_mark(kProfTsqrLeaf, true, st);
+  tsqr_split_leaf_kernel<<<nleaves, 256, smem, st>>>(x, m, ldx, rpc, sg, slots, stats, wsr);
+  TSNMF_LAUNCH_CHECK();
+  prof_mark(kProfTsqrLeaf, false, st);
+  return kOk;
+}
+
 }  // namespace
 
 int tsqr_max_cols() { return 512; }
@@ -1509,12 +1849,17 @@ size_t tsqr_workspace_bytes(int64_t m, int n) {
   if (n < 1 || !tq_config(n, &ch)) return 0;
   int nleaves;
   int64_t rpc;
-  if (small_path(n))
+  size_t extra = 0;
+  if (small_path(n)) {
     narrow_plan(n, max64(m, 1), &nleaves, &rpc);
-  else
+  } else if (split_path(n)) {
+    split_plan(n, max64(m, 1), &nleaves, &rpc);
+    extra = split_ws_doubles(split_geom(n), nleaves);
+  } else {
     tq_plan(ch, max64(m, 1), &nleaves, &rpc);
+  }
   const int64_t npad = ch.g.npad;
-  return sizeof(double) * (size_t)(nleaves * npad * npad + nleaves * 2 * npad) + 256;
+  return sizeof(double) * ((size_t)(nleaves * npad * npad + nleaves * 2 * npad) + extra) + 256;
 }
 
 size_t combine_workspace_bytes(int count, int n) {
@@ -1531,12 +1876,18 @@ int tsqr_run(const double* x, int64_t m, int n, int64_t ldx, double* r, int64_t 
   int nleaves;
   int64_t rpc;
   const bool narrow = small_path(n);
-  if (narrow)
+  const bool split = !narrow && split_path(n);
+  size_t extra = 0;
+  if (narrow) {
     narrow_plan(n, m, &nleaves, &rpc);
-  else
+  } else if (split) {
+    split_plan(n, m, &nleaves, &rpc);
+    extra = split_ws_doubles(split_geom(n), nleaves);
+  } else {
     tq_plan(ch, m, &nleaves, &rpc);
+  }
   const int64_t npad = ch.g.npad;
-  const size_t need = sizeof(double) * (size_t)(nleaves * npad * npad + nleaves * 2 * npad);
+  const size_t need = sizeof(double) * ((size_t)(nleaves * npad * npad + nleaves * 2 * npad) + extra);
   if (ws_bytes < need) return set_error(kUsage, "tsqr: workspace too small (%zu < %zu bytes)", ws_bytes, need);
   double* slots = reinterpret_cast<double*>(ws);
   double* stats = slots + (int64_t)nleaves * npad * npad;
@@ -1546,6 +1897,10 @@ int tsqr_run(const double* x, int64_t m, int n, int64_t ldx, double* r, int64_t 
     rc = warp_leaf(x, m, n, ldx, rpc, nleaves, slots, want_stats ? stats : nullptr, st);
   } else if (narrow) {
     rc = small_leaf(x, m, n, ldx, rpc, nleaves, (int)npad, slots, want_stats ? stats : nullptr, st);
+  } else if (split) {
+    double* wsr = stats + (int64_t)nleaves * 2 * npad;
+    rc = split_leaf(x, m, ldx, split_geom(n), nleaves, rpc, slots, want_stats ? stats : nullptr, wsr, st);
+    if (!rc) rc = tq_dispatch(ch, nullptr, 0, 0, slots, nullptr, nleaves, 0, st);  // the combine tree
   } else {
     rc = tq_dispatch(ch, x, m, ldx, slots, want_stats ? stats : nullptr, nleaves, rpc, st);
   }
@@ -1593,6 +1948,13 @@ int tsqr_describe(int n, int64_t m, int* nb, int* brows, int* ctas_per_sm, int* 
     *nb = 1;
     *brows = 32;
     *ctas_per_sm = 3;
+    return kOk;
+  }
+  if (split_path(n)) {  // split leaf: 256-row blocks, one CTA per SM
+    split_plan(n, max64(m, 1), nleaves, &rpc);
+    *nb = kNB;
+    *brows = kSplitRows;
+    *ctas_per_sm = 1;
     return kOk;
   }
   tq_plan(ch, max64(m, 1), nleaves, &rpc);
