@@ -20,7 +20,11 @@
 // reference TreeReducer order (perfect binary levels over the leaf index, then a fold of the leftover
 // subtrees), each combine being the same structured QR with the second factor's rows as data
 // (triangular: panels left of the block are skipped).
+#include <algorithm>
+#include <map>
+#include <mutex>
 #include <utility>
+#include <vector>
 
 #include "common.cuh"
 #include "internal.h"
@@ -62,6 +66,11 @@ __device__ __forceinline__ int swz(int row) { return (row & 2) << 1; }
 constexpr int kBarColsReady = 1;  // next panel's columns updated + its R rows staged  (GEMM, helper -> panel)
 constexpr int kBarPanelDone = 2;  // V, T of the current panel published               (panel -> GEMM, helper)
 constexpr int kBarPanelPair = 4;  // panel warp + helper (pair lookahead partials)
+// Lookahead tile ready (64 threads): the panel warp starts its half of the pair lookahead of panel p on tile
+// p + 1 right after publishing panel p, i.e. possibly while the GEMM warps still run iteration p - 1, whose
+// update of tile p + 1 by panel p - 1 it must see.  The GEMM warp that applies that update arrives here
+// after it; the panel warp syncs before the lookahead.  (Without it the order held only by timing.)
+constexpr int kBarNextReady = 5;
 constexpr int kGemmWarps = 6;
 __device__ __forceinline__ void named_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
@@ -654,6 +663,7 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
         TQ_TRACE(2);
         named_arrive(kBarPanelDone, kThr);
         if (kPairLookahead && more) {
+          if (p > p0) named_sync(kBarNextReady, 64);  // tile p + 1's update by panel p - 1 is done
           __syncwarp();  // the warp's own V / T stores are visible to all its lanes
           lookahead_pair(Bs, lds, brows, j0, j0, R, npad, Tmc, Wpart, Wsc, p + 1, 8 * (p + 1), 0, lane);
         }
@@ -705,6 +715,11 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
             const int one[1] = {cbs[0]};
             const int pc[1] = {8 * cbs[0]};
             update_cbs<1>(Bs, lds, brows, j0, j0, R, npad, Tmc, Wsc, one, pc, lane, tq_p);
+          }
+          // tile p + 2 (this warp's first group when gi == 0) is the next lookahead's target
+          if (kPairLookahead && base == p + 2) {
+            __syncwarp();
+            named_arrive(kBarNextReady, 64);
           }
         }
       }
@@ -791,48 +806,66 @@ __host__ __device__ inline TqGeom split_tq_geom(const SplitGeom& sg) {
 }
 
 // One right tile (logical column block cb) updated with panel (j0)'s block reflector, data streamed from
-// global memory (X when kFromX, else the workspace) and written to the workspace (or, kToSmem, to the
-// swizzled shared slot at column dcol).  Lane l holds the tile in the DMMA B-operand layout (row 4s + l%4,
-// col l/4 in register s) for W = R_p + V^T B; the C-tile layout of B -= V W' (row l/4, cols 2(l%4)..+1)
-// is gathered from those registers by shuffles, so the tile is read from L2 once.
+// global memory (X when kFromX, else the tile's workspace slot: tile-major, 256 rows x 8 doubles) and
+// written to the workspace slot (or, kToSmem, to the swizzled shared slot at column dcol).  Lane l holds
+// the tile in the DMMA B-operand layout (row 4s + l%4, col l/4 in register s) for W = R_p + V^T B; the
+// C-tile layout of B -= V W' (row l/4, cols 2(l%4)..+1) is gathered from those registers by shuffles, so the
+// tile is read from L2 once.  kFromX also adds the tile's column l1 / sum of squares to st[0..8) / st[8..16)
+// (one warp owns a right tile's first update, so plain read-modify-writes).  Not inlined: one copy of each
+// variant instead of one per call site keeps the kernel inside the instruction cache.
 template <bool kFromX, bool kToSmem>
-__device__ __forceinline__ void update_global(const double* __restrict__ Bs, int lds, int vj, int j0,
-                                              const double* __restrict__ src, int64_t lsrc, int vrows, int vcols,
-                                              double* __restrict__ dst, int64_t ldst, double* __restrict__ Bd,
-                                              int dcol, double* __restrict__ R, int npad, int cb,
-                                              const double* __restrict__ Tm, double* __restrict__ Wsc, int lane,
-                                              double& sa, double& sq) {
+__device__ __noinline__ void update_global(const double* __restrict__ Bs, int lds, int vj, int j0,
+                                           const double* __restrict__ src, int64_t ldx, int vrows, int vcols,
+                                           double* __restrict__ dst, int dcol, double* __restrict__ R, int npad,
+                                           int cb, const double* __restrict__ Tm, double* __restrict__ Wsc,
+                                           double* __restrict__ st) {
   constexpr int K = kSplitRows / 4;  // k-steps (registers per lane)
+  const int lane = threadIdx.x & 31;
   const int frag_col = (lane >> 2) ^ ((lane & 2) << 1);
   const int vsw = ((lane >> 2) & 2) << 1;
   double* rtile = R + (int64_t)(j0 + (lane >> 2)) * npad + 8 * cb + 2 * (lane & 3);
   const double2 rinit = *reinterpret_cast<const double2*>(rtile);
   double b[K];
-  {
-    const double* bp = src + (int64_t)(lane & 3) * lsrc + (lane >> 2);
-    const bool colok = !kFromX || (lane >> 2) < vcols;
+  if (kFromX) {
+    const double* bp = src + (int64_t)(lane & 3) * ldx + (lane >> 2);
+    const bool colok = (lane >> 2) < vcols;
+    const int64_t step = 4 * ldx;
 #pragma unroll
     for (int s = 0; s < K; ++s) {
-      const int row = 4 * s + (lane & 3);
-      if (kFromX)
-        b[s] = (colok && row < vrows) ? __ldcs(bp + (int64_t)4 * s * lsrc) : 0.0;
-      else
-        b[s] = __ldcg(bp + (int64_t)4 * s * lsrc);
+      b[s] = (colok && 4 * s + (lane & 3) < vrows) ? __ldcs(bp) : 0.0;
+      bp += step;
     }
+  } else {
+    const double* bp = src + 8 * (lane & 3) + (lane >> 2);
+#pragma unroll
+    for (int s = 0; s < K; ++s) b[s] = __ldcg(bp + 32 * s);
   }
-  double c[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+  // two accumulator chains over alternating 4-row k-steps, summed (c0 + c1) + R: update_cbs's order, so a
+  // tile's update is bitwise the same whichever path applies it
+  double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
   const double* vslab = Bs + (lane & 3) * lds + frag_col + vj;
+  double sa = 0.0, sq = 0.0;
 #pragma unroll
   for (int s = 0; s < K; ++s) {
-    dmma(c[s & 3][0], c[s & 3][1], vslab[4 * s * lds], b[s]);
+    dmma(c[s & 1][0], c[s & 1][1], vslab[4 * s * lds], b[s]);
     if (kFromX) {
       sa += fabs(b[s]);
       sq = fma(b[s], b[s], sq);
     }
   }
+  if (kFromX) {
+    sa += __shfl_xor_sync(0xffffffffu, sa, 1);
+    sq += __shfl_xor_sync(0xffffffffu, sq, 1);
+    sa += __shfl_xor_sync(0xffffffffu, sa, 2);
+    sq += __shfl_xor_sync(0xffffffffu, sq, 2);
+    if ((lane & 3) == 0) {
+      st[lane >> 2] += sa;
+      st[8 + (lane >> 2)] += sq;
+    }
+  }
   const int ci = (lane >> 2) * 8 + 2 * (lane & 3);
-  Wsc[ci] = ((c[0][0] + c[1][0]) + (c[2][0] + c[3][0])) + rinit.x;
-  Wsc[ci + 1] = ((c[0][1] + c[1][1]) + (c[2][1] + c[3][1])) + rinit.y;
+  Wsc[ci] = (c[0][0] + c[1][0]) + rinit.x;
+  Wsc[ci + 1] = (c[0][1] + c[1][1]) + rinit.y;
   __syncwarp();
   double w0 = 0.0, w1 = 0.0;
 #pragma unroll
@@ -849,6 +882,8 @@ __device__ __forceinline__ void update_global(const double* __restrict__ Bs, int
   // C tile of row block rb: element (8 rb + l/4, c) is register 2 rb + (l >> 4) of lane 4 c + (l/4) % 4
   const int src0 = 8 * (lane & 3) + ((lane >> 2) & 3);
   const bool hi = (lane >> 4) != 0;
+  const double* vrow = Bs + (lane >> 2) * lds + vj;
+  const int va = (lane & 3) ^ vsw, vb = (4 + (lane & 3)) ^ vsw;
 #pragma unroll
   for (int rb = 0; rb < kSplitRows / 8; ++rb) {
     const double x0a = __shfl_sync(0xffffffffu, b[2 * rb], src0);
@@ -856,14 +891,14 @@ __device__ __forceinline__ void update_global(const double* __restrict__ Bs, int
     const double x1a = __shfl_sync(0xffffffffu, b[2 * rb], src0 + 4);
     const double x1b = __shfl_sync(0xffffffffu, b[2 * rb + 1], src0 + 4);
     double cx = hi ? x0b : x0a, cy = hi ? x1b : x1a;
-    const int row = 8 * rb + (lane >> 2);
-    const double* vrow = Bs + row * lds + vj;
-    dmma(cx, cy, vrow[(lane & 3) ^ vsw], wb0);
-    dmma(cx, cy, vrow[(4 + (lane & 3)) ^ vsw], wb1);
+    const double* vr = vrow + 8 * rb * lds;
+    dmma(cx, cy, vr[va], wb0);
+    dmma(cx, cy, vr[vb], wb1);
     if (kToSmem)
-      *reinterpret_cast<double2*>(Bd + row * lds + dcol + ((2 * (lane & 3)) ^ vsw)) = make_double2(cx, cy);
+      *reinterpret_cast<double2*>(dst + (8 * rb + (lane >> 2)) * lds + dcol + ((2 * (lane & 3)) ^ vsw)) =
+          make_double2(cx, cy);
     else
-      __stcg(reinterpret_cast<double2*>(dst + (int64_t)row * ldst + 2 * (lane & 3)), make_double2(cx, cy));
+      __stcg(reinterpret_cast<double2*>(dst + 64 * rb + 8 * (lane >> 2) + 2 * (lane & 3)), make_double2(cx, cy));
   }
 }
 
@@ -888,6 +923,7 @@ __device__ void tsqr_split_fold(double* __restrict__ R, const double* __restrict
   double* red = smem + L::red(g);
   double* Wsc = smem + L::wsc(g) + warp * kNB * 8;
   double* Wpart = smem + L::wpart(g);
+  double* rstat = smem + L::total(g);  // right tile t - S: column l1 [16 (t - S), +8), sum of squares [+8, +16)
   const bool vec16 = ((ldx & 1) == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
   const int scols = ncols < lcols ? ncols : lcols;
   auto slot_col = [&](int t) { return 8 * (t < S ? t : t - S); };
@@ -897,10 +933,7 @@ __device__ void tsqr_split_fold(double* __restrict__ R, const double* __restrict
   double l1a[kSH], sqa[kSH];
 #pragma unroll
   for (int h = 0; h < kSH; ++h) l1a[h] = sqa[h] = 0.0;
-  // right-tile stats: the GEMM warp that updates right tile t in iteration 0 (t = 2 + gi + kGemm * gg)
-  double rsa[G], rsq[G];
-#pragma unroll
-  for (int gg = 0; gg < G; ++gg) rsa[gg] = rsq[gg] = 0.0;
+  for (int i = tid; i < 2 * sg.wld; i += kThr) rstat[i] = 0.0;  // (ordered by the block loop's barrier)
   const int gi = warp == 0 || warp == kHelper ? -1 : gemm_index(warp);
 
   for (int64_t r0 = 0; r0 < nrows; r0 += brows) {
@@ -910,7 +943,7 @@ __device__ void tsqr_split_fold(double* __restrict__ R, const double* __restrict
     stage_block(Bs, lds, xb, ldx, cnt, scols, brows, lcols, vec16);
     if (warp == 0) stage_rdiag(Rdg, R, npad, 0, lane);
     cp_async_commit();
-    // the next block's right columns into L2 (its first trailing update reads X)
+    // the next block's right columns into L2 (right tiles' first updates read X)
     if (r0 + brows < nrows && ncols > lcols) {
       const int64_t nrow0 = r0 + brows;
       const int nr = (int)min64(brows, nrows - nrow0);
@@ -946,65 +979,77 @@ __device__ void tsqr_split_fold(double* __restrict__ R, const double* __restrict
       const double* Rdc = Rdg + buf * kNB * kNB;
       const double* Tmc = Tm + buf * kNB * kNB;
       const bool more = p + 1 < npanels;
-      const int tq_p = -1;
+      const int tq_p = (r0 == brows && p < 64) ? p : -1;  // trace builds: the second block of CTA 0
       if (warp == 0) {
         if (p > 0) named_sync(kBarColsReady, kThr);
-        panel_factor_lazy<RQ, true>(Bs, lds, brows, j0, vj, R, npad, Rdc, Tm + buf * kNB * kNB, red, lane, tq_p);
+        TQ_RESOLVE(Rdg);
+        TQ_TRACE(41);
+        panel_factor_lazy<RQ, true>(Bs, lds, brows, j0, vj, R, npad, Rdc, Tm + buf * kNB * kNB, red, lane, -1);
+        TQ_TRACE(42);
         named_arrive(kBarPanelDone, kThr);
         if (more) {
+          if (p > 0) named_sync(kBarNextReady, 64);  // tile p + 1's update by panel p - 1 is done
           __syncwarp();
           lookahead_pair(Bs, lds, brows, j0, vj, R, npad, Tmc, Wpart, Wsc, p + 1, slot_col(p + 1), 0, lane);
+          TQ_TRACE(45);
         }
       } else if (warp == kHelper) {
         named_sync(kBarPanelDone, kThr);
+        TQ_RESOLVE(Rdg);
+        TQ_TRACE(43);
         if (more) {
           stage_rdiag(Rdg + (buf ^ 1) * kNB * kNB, R, npad, j0 + kNB, lane);
           cp_async_commit();
           lookahead_pair(Bs, lds, brows, j0, vj, R, npad, Tmc, Wpart, Wsc, p + 1, slot_col(p + 1), 1, lane);
           cp_async_wait<0>();
           __syncwarp();
+          TQ_TRACE(44);
           named_arrive(kBarColsReady, kThr);
         }
       } else {
         named_sync(kBarPanelDone, kThr);
+        TQ_RESOLVE(Rdg);
+        TQ_TRACE(46);
         if (more) named_arrive(kBarColsReady, kThr);
         for (int base = p + 2 + gi; base < npanels; base += kGemm * G) {
-          // shared tiles of this group in one call (shared V fragment loads); workspace tiles one by one.
-          // Tiles in shared memory are those below S + max(p - 1, 0): a prefix of the group.
+          // shared tiles of this group in one call (shared V fragment loads), then the workspace tiles one by
+          // one.  Tiles in shared memory are those below S + max(p - 1, 0): a prefix of the group.
           const int lim = min(npanels, S + (p > 0 ? p - 1 : 0));
           const int c4[4] = {base, base + kGemm, base + 2 * kGemm, base + 3 * kGemm};
           const int ns = c4[3] < lim ? 4 : (c4[2] < lim ? 3 : (c4[1] < lim ? 2 : (c4[0] < lim ? 1 : 0)));
           if (ns == 4) {
             const int p4[4] = {slot_col(c4[0]), slot_col(c4[1]), slot_col(c4[2]), slot_col(c4[3])};
-            update_cbs<4>(Bs, lds, brows, j0, vj, R, npad, Tmc, Wsc, c4, p4, lane, tq_p);
+            update_cbs<4>(Bs, lds, brows, j0, vj, R, npad, Tmc, Wsc, c4, p4, lane, -1);
           } else if (ns == 3) {
             const int c3[3] = {c4[0], c4[1], c4[2]}, p3[3] = {slot_col(c4[0]), slot_col(c4[1]), slot_col(c4[2])};
-            update_cbs<3>(Bs, lds, brows, j0, vj, R, npad, Tmc, Wsc, c3, p3, lane, tq_p);
+            update_cbs<3>(Bs, lds, brows, j0, vj, R, npad, Tmc, Wsc, c3, p3, lane, -1);
           } else if (ns == 2) {
             const int c2[2] = {c4[0], c4[1]}, p2[2] = {slot_col(c4[0]), slot_col(c4[1])};
-            update_cbs<2>(Bs, lds, brows, j0, vj, R, npad, Tmc, Wsc, c2, p2, lane, tq_p);
+            update_cbs<2>(Bs, lds, brows, j0, vj, R, npad, Tmc, Wsc, c2, p2, lane, -1);
           } else if (ns == 1) {
             const int c1[1] = {c4[0]}, p1[1] = {slot_col(c4[0])};
-            update_cbs<1>(Bs, lds, brows, j0, vj, R, npad, Tmc, Wsc, c1, p1, lane, tq_p);
+            update_cbs<1>(Bs, lds, brows, j0, vj, R, npad, Tmc, Wsc, c1, p1, lane, -1);
           }
-#pragma unroll
-          for (int gg = 0; gg < G; ++gg) {
+          if (base == p + 2) {  // tile p + 2 (gi == 0, shared slot) is the next lookahead's target
+            __syncwarp();
+            named_arrive(kBarNextReady, 64);
+          }
+          TQ_TRACE(47);
+#pragma unroll 1
+          for (int gg = ns; gg < G; ++gg) {
             const int t = base + kGemm * gg;
-            if (t >= npanels || t < lim) continue;
-            double* wt = ws + 8 * (t - S);
-            if (p == 0) {
-              update_global<true, false>(Bs, lds, vj, j0, xb + 8 * t, ldx, cnt, ncols - 8 * t, wt, sg.wld, nullptr,
-                                         0, R, npad, t, Tmc, Wsc, lane, rsa[gg], rsq[gg]);
-            } else if (t - S + 1 == p) {
-              double d0 = 0.0, d1 = 0.0;
-              update_global<false, true>(Bs, lds, vj, j0, wt, sg.wld, brows, 8, nullptr, 0, Bs, 8 * (t - S), R,
-                                         npad, t, Tmc, Wsc, lane, d0, d1);
-            } else {
-              double d0 = 0.0, d1 = 0.0;
-              update_global<false, false>(Bs, lds, vj, j0, wt, sg.wld, brows, 8, wt, sg.wld, nullptr, 0, R, npad,
-                                          t, Tmc, Wsc, lane, d0, d1);
-            }
+            if (t >= npanels) break;
+            double* wt = ws + (int64_t)kSplitRows * 8 * (t - S);  // tile-major workspace slot
+            if (p == 0)
+              update_global<true, false>(Bs, lds, vj, j0, xb + 8 * t, ldx, cnt, ncols - 8 * t, wt, 0, R, npad, t,
+                                         Tmc, Wsc, rstat + 16 * (t - S));
+            else if (t - S + 1 == p)
+              update_global<false, true>(Bs, lds, vj, j0, wt, 0, 0, 0, Bs, 8 * (t - S), R, npad, t, Tmc, Wsc,
+                                         nullptr);
+            else
+              update_global<false, false>(Bs, lds, vj, j0, wt, 0, 0, 0, wt, 0, R, npad, t, Tmc, Wsc, nullptr);
           }
+          TQ_TRACE(48);
         }
       }
     }
@@ -1018,20 +1063,11 @@ __device__ void tsqr_split_fold(double* __restrict__ R, const double* __restrict
         stats_out[npad + col] = sqa[h];
       }
     }
-    if (gi >= 0) {
-#pragma unroll
-      for (int gg = 0; gg < G; ++gg) {
-        double a = rsa[gg], q = rsq[gg];
-        a += __shfl_xor_sync(0xffffffffu, a, 1);
-        q += __shfl_xor_sync(0xffffffffu, q, 1);
-        a += __shfl_xor_sync(0xffffffffu, a, 2);
-        q += __shfl_xor_sync(0xffffffffu, q, 2);
-        const int t = 2 + gi + kGemm * gg;
-        if (t >= S && t < npanels && (lane & 3) == 0) {
-          stats_out[8 * t + (lane >> 2)] = a;
-          stats_out[npad + 8 * t + (lane >> 2)] = q;
-        }
-      }
+    __syncthreads();
+    for (int i = tid; i < 8 * (npanels - S); i += kThr) {
+      const int t = S + i / 8, c = i % 8;
+      stats_out[8 * t + c] = rstat[16 * (t - S) + c];
+      stats_out[npad + 8 * t + c] = rstat[16 * (t - S) + 8 + c];
     }
   }
 }
@@ -1803,7 +1839,7 @@ SplitGeom split_geom(int n) {
   sg.wld = 8 * (np - sg.S);
   return sg;
 }
-size_t split_smem(const SplitGeom& sg) { return TqLayout::bytes(split_tq_geom(sg)); }
+size_t split_smem(const SplitGeom& sg) { return TqLayout::bytes(split_tq_geom(sg)) + sizeof(double) * 2 * sg.wld; }  // + right-tile stats
 void split_plan(int n, int64_t m, int* nleaves, int64_t* rows_per_cta) {
   const int64_t npad = round_up(n, kNB);
   const int64_t max_leaves = device_sms();
@@ -1813,7 +1849,9 @@ void split_plan(int n, int64_t m, int* nleaves, int64_t* rows_per_cta) {
   *nleaves = (int)ceil_div(m, rpc);
   *rows_per_cta = rpc;
 }
+// workspace after the R slots and stats: the right tiles (nleaves x 256 x wld, tile-major)
 size_t split_ws_doubles(const SplitGeom& sg, int nleaves) { return (size_t)nleaves * kSplitRows * sg.wld; }
+
 int split_leaf(const double* x, int64_t m, int64_t ldx, const SplitGeom& sg, int nleaves, int64_t rpc,
                double* slots, double* stats, double* wsr, cudaStream_t st) {
   static PerDeviceFlag attr;
