@@ -359,6 +359,28 @@ __device__ __forceinline__ double rcp_nb(double a) {
   return y * sc;
 }
 
+// L2 eviction-priority policies (createpolicy) and hinted global accesses: streamed-once data (X) is
+// evict_first so it does not push out the re-used working set (TSQR R slots, split-leaf workspace tiles),
+// which is evict_last.
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ double ld_hint(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_hint(double2* p, double2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
+}
+
 // cp.async helpers (LDGSTS): global -> shared without staging through registers.
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -367,6 +389,14 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16_hint(void* smem, const void* gmem, uint64_t pol) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "l"(pol));
+}
+__device__ __forceinline__ void cp_async8_hint(void* smem, const void* gmem, uint64_t pol) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "l"(pol));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
@@ -433,21 +463,31 @@ struct GridWalk {
 // stride lds (swizzled: column c of row r at r*lds + swz_col(r, c)); rows [nrows, rows_total) and cols
 // [ncols, cols_total) are zero-filled.  cols_total must be a multiple of 8.  All threads of the CTA
 // participate; the caller commits / waits.
-template <bool kSwz>
+template <bool kSwz, bool kStream = false>
 __device__ __forceinline__ void stage_rows_impl(double* __restrict__ dst, int lds, const double* __restrict__ src,
                                                 int64_t ldsrc, int nrows, int ncols, int rows_total,
                                                 int cols_total, bool vec16) {
   const int tid = threadIdx.x, nth = blockDim.x;
   auto at = [&](int r, int c) -> double* { return dst + (int64_t)r * lds + (kSwz ? swz_col(r, c) : c); };
+  const uint64_t pol = kStream ? l2_policy_evict_first() : 0;
   if (vec16) {
     const int pairs = ncols >> 1;
     if (pairs > 0)
-      for (GridWalk it(tid, nth, pairs); it.r < nrows; it.next())
-        cp_async16(at(it.r, 2 * it.c), src + it.r * ldsrc + 2 * it.c);
+      for (GridWalk it(tid, nth, pairs); it.r < nrows; it.next()) {
+        if (kStream)
+          cp_async16_hint(at(it.r, 2 * it.c), src + it.r * ldsrc + 2 * it.c, pol);
+        else
+          cp_async16(at(it.r, 2 * it.c), src + it.r * ldsrc + 2 * it.c);
+      }
     if (ncols & 1)
       for (int r = tid; r < nrows; r += nth) cp_async8(at(r, ncols - 1), src + r * ldsrc + ncols - 1);
   } else if (ncols > 0) {
-    for (GridWalk it(tid, nth, ncols); it.r < nrows; it.next()) cp_async8(at(it.r, it.c), src + it.r * ldsrc + it.c);
+    for (GridWalk it(tid, nth, ncols); it.r < nrows; it.next()) {
+      if (kStream)
+        cp_async8_hint(at(it.r, it.c), src + it.r * ldsrc + it.c, pol);
+      else
+        cp_async8(at(it.r, it.c), src + it.r * ldsrc + it.c);
+    }
   }
   const int pad = cols_total - ncols;
   if (pad > 0)
@@ -460,6 +500,12 @@ __device__ __forceinline__ void stage_rows_swz(double* __restrict__ dst, int lds
                                                int64_t ldsrc, int nrows, int ncols, int rows_total,
                                                int cols_total, bool vec16) {
   stage_rows_impl<true>(dst, lds, src, ldsrc, nrows, ncols, rows_total, cols_total, vec16);
+}
+// the same for streamed-once input (L2 evict_first)
+__device__ __forceinline__ void stage_rows_swz_stream(double* __restrict__ dst, int lds, const double* __restrict__ src,
+                                                      int64_t ldsrc, int nrows, int ncols, int rows_total,
+                                                      int cols_total, bool vec16) {
+  stage_rows_impl<true, true>(dst, lds, src, ldsrc, nrows, ncols, rows_total, cols_total, vec16);
 }
 
 }  // namespace tsnmf

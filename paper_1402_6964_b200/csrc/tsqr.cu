@@ -786,7 +786,10 @@ __global__ void __launch_bounds__(32 * tq_warps<MINB>(), MINB)
 // in shared memory (S >= 3).  Logical tile t lives in slot t (t < S) or t - S (t >= S, migrated);
 // R is addressed logically.  The first update of a right tile reads X directly (zero-filling rows past
 // the end and padding columns) and accumulates its column l1 / sum of squares on the way.
-constexpr int kSplitRows = 256;
+#ifndef TSNMF_SPLIT_ROWS
+#define TSNMF_SPLIT_ROWS 256
+#endif
+constexpr int kSplitRows = TSNMF_SPLIT_ROWS;  // multiple of 32 (panel rows per lane = kSplitRows / 32)
 constexpr int kSplitRq = kSplitRows / 32;
 
 struct SplitGeom {
@@ -821,6 +824,7 @@ __device__ __noinline__ void update_global(const double* __restrict__ Bs, int ld
                                            double* __restrict__ st) {
   constexpr int K = kSplitRows / 4;  // k-steps (registers per lane)
   const int lane = threadIdx.x & 31;
+  const uint64_t pol_ws = l2_policy_evict_last(), pol_x = l2_policy_evict_first();
   const int frag_col = (lane >> 2) ^ ((lane & 2) << 1);
   const int vsw = ((lane >> 2) & 2) << 1;
   double* rtile = R + (int64_t)(j0 + (lane >> 2)) * npad + 8 * cb + 2 * (lane & 3);
@@ -832,13 +836,13 @@ __device__ __noinline__ void update_global(const double* __restrict__ Bs, int ld
     const int64_t step = 4 * ldx;
 #pragma unroll
     for (int s = 0; s < K; ++s) {
-      b[s] = (colok && 4 * s + (lane & 3) < vrows) ? __ldcs(bp) : 0.0;
+      b[s] = (colok && 4 * s + (lane & 3) < vrows) ? ld_hint(bp, pol_x) : 0.0;
       bp += step;
     }
   } else {
     const double* bp = src + 8 * (lane & 3) + (lane >> 2);
 #pragma unroll
-    for (int s = 0; s < K; ++s) b[s] = __ldcg(bp + 32 * s);
+    for (int s = 0; s < K; ++s) b[s] = ld_hint(bp + 32 * s, pol_ws);
   }
   // two accumulator chains over alternating 4-row k-steps, summed (c0 + c1) + R: update_cbs's order, so a
   // tile's update is bitwise the same whichever path applies it
@@ -898,7 +902,24 @@ __device__ __noinline__ void update_global(const double* __restrict__ Bs, int ld
       *reinterpret_cast<double2*>(dst + (8 * rb + (lane >> 2)) * lds + dcol + ((2 * (lane & 3)) ^ vsw)) =
           make_double2(cx, cy);
     else
-      __stcg(reinterpret_cast<double2*>(dst + 64 * rb + 8 * (lane >> 2) + 2 * (lane & 3)), make_double2(cx, cy));
+      st_hint(reinterpret_cast<double2*>(dst + 64 * rb + 8 * (lane >> 2) + 2 * (lane & 3)), make_double2(cx, cy), pol_ws);
+  }
+}
+
+#ifndef TSNMF_SPLIT_PREFETCH
+#define TSNMF_SPLIT_PREFETCH 0  // measured: none 265, at block start 261, late 261 GB/s (C2 shape, 2^24 rows)
+#endif
+constexpr int kSplitPrefetch = TSNMF_SPLIT_PREFETCH;  // next block's right columns into L2: 0 off, 1 at block start, 2 late
+// L2 prefetch of the right columns [lcols, ncols) of rows [row0, row0 + 256) (their first updates read X)
+__device__ __forceinline__ void prefetch_next_right(const double* X, int64_t ldx, int64_t nrows, int64_t row0,
+                                                    int lcols, int ncols, int t, int nt) {
+  if (row0 >= nrows || ncols <= lcols) return;
+  const int nr = (int)min64(kSplitRows, nrows - row0);
+  for (int r = t; r < nr; r += nt) {
+    const char* a = reinterpret_cast<const char*>(X + (row0 + r) * ldx + lcols);
+    const char* e = reinterpret_cast<const char*>(X + (row0 + r) * ldx + ncols);
+    for (const char* q = (const char*)((uintptr_t)a & ~(uintptr_t)127); q < e; q += 128)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
   }
 }
 
@@ -940,20 +961,10 @@ __device__ void tsqr_split_fold(double* __restrict__ R, const double* __restrict
     const int cnt = (int)min64(brows, nrows - r0);
     const double* xb = X + r0 * ldx;
     __syncthreads();
-    stage_block(Bs, lds, xb, ldx, cnt, scols, brows, lcols, vec16);
+    stage_rows_swz_stream(Bs, lds, xb, ldx, cnt, scols, brows, lcols, vec16);
     if (warp == 0) stage_rdiag(Rdg, R, npad, 0, lane);
     cp_async_commit();
-    // the next block's right columns into L2 (right tiles' first updates read X)
-    if (r0 + brows < nrows && ncols > lcols) {
-      const int64_t nrow0 = r0 + brows;
-      const int nr = (int)min64(brows, nrows - nrow0);
-      for (int r = tid; r < nr; r += kThr) {
-        const char* a = reinterpret_cast<const char*>(X + (nrow0 + r) * ldx + lcols);
-        const char* e = reinterpret_cast<const char*>(X + (nrow0 + r) * ldx + ncols);
-        for (const char* q = (const char*)((uintptr_t)a & ~(uintptr_t)127); q < e; q += 128)
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
-      }
-    }
+    if (kSplitPrefetch == 1) prefetch_next_right(X, ldx, nrows, r0 + brows, lcols, ncols, tid, kThr);
     cp_async_wait<0>();
     __syncthreads();
     if (stats_out) {
@@ -980,6 +991,8 @@ __device__ void tsqr_split_fold(double* __restrict__ R, const double* __restrict
       const double* Tmc = Tm + buf * kNB * kNB;
       const bool more = p + 1 < npanels;
       const int tq_p = (r0 == brows && p < 64) ? p : -1;  // trace builds: the second block of CTA 0
+      if (kSplitPrefetch == 2 && p == npanels - 6 && gi >= 0)  // GEMM warps, off the tail of the block
+        prefetch_next_right(X, ldx, nrows, r0 + brows, lcols, ncols, tid - 32 * (warp < kHelper ? 1 : 2), 32 * kGemm);
       if (warp == 0) {
         if (p > 0) named_sync(kBarColsReady, kThr);
         TQ_RESOLVE(Rdg);
@@ -1829,17 +1842,22 @@ bool split_path(int n) {
   if (const char* e = getenv("TSNMF_TSQR_SPLIT")) return atoi(e) != 0;
   return true;
 }
+size_t split_smem(const SplitGeom& sg) { return TqLayout::bytes(split_tq_geom(sg)) + sizeof(double) * 2 * sg.wld; }  // + right-tile stats
+// as many shared slots as fit (fewer workspace tiles); at least half the tiles so every right tile t has
+// its own slot t - S to move into
 SplitGeom split_geom(int n) {
   SplitGeom sg;
   sg.n = n;
   sg.npad = (int)round_up(n, kNB);
   const int np = sg.npad / kNB;
-  sg.S = (np + 1) / 2;
-  sg.lds = smem_stride(8 * sg.S);
-  sg.wld = 8 * (np - sg.S);
+  for (int S = np; S >= (np + 1) / 2; --S) {
+    sg.S = S;
+    sg.lds = smem_stride(8 * S);
+    sg.wld = 8 * (np - S);
+    if (split_smem(sg) <= 232448 - 1024 || S == (np + 1) / 2) break;
+  }
   return sg;
 }
-size_t split_smem(const SplitGeom& sg) { return TqLayout::bytes(split_tq_geom(sg)) + sizeof(double) * 2 * sg.wld; }  // + right-tile stats
 void split_plan(int n, int64_t m, int* nleaves, int64_t* rows_per_cta) {
   const int64_t npad = round_up(n, kNB);
   const int64_t max_leaves = device_sms();
