@@ -810,51 +810,57 @@ __host__ __device__ inline TqGeom split_tq_geom(const SplitGeom& sg) {
 
 // One right tile (logical column block cb) updated with panel (j0)'s block reflector, data streamed from
 // global memory (X when kFromX, else the tile's workspace slot: tile-major, 256 rows x 8 doubles) and
-// written to the workspace slot (or, kToSmem, to the swizzled shared slot at column dcol).  Lane l holds
-// the tile in the DMMA B-operand layout (row 4s + l%4, col l/4 in register s) for W = R_p + V^T B; the
-// C-tile layout of B -= V W' (row l/4, cols 2(l%4)..+1) is gathered from those registers by shuffles, so the
-// tile is read from L2 once.  kFromX also adds the tile's column l1 / sum of squares to st[0..8) / st[8..16)
-// (one warp owns a right tile's first update, so plain read-modify-writes).  Not inlined: one copy of each
-// variant instead of one per call site keeps the kernel inside the instruction cache.
+// written to the workspace slot (or, kToSmem, to the swizzled shared slot at column dcol).  The W pass
+// (W = R_p + V^T B) takes the tile in the DMMA B-operand layout (lane: row 4s + l%4, col l/4), all of it in
+// flight at once; the C pass (B -= V W') re-reads it in the C-tile layout (row l/4, cols 2(l%4)..+1: 512
+// contiguous bytes per 8 rows, L2 hits) in double-buffered batches instead of regathering registers with
+// shuffles.  kFromX also adds the tile's column l1 / sum of squares to st[0..8) / st[8..16) (one warp owns a
+// right tile's first update, so plain read-modify-writes).  Not inlined: one copy per variant keeps the
+// kernel in the instruction cache and its register budget for the panel / update_cbs paths.
 template <bool kFromX, bool kToSmem>
 __device__ __noinline__ void update_global(const double* __restrict__ Bs, int lds, int vj, int j0,
-                                           const double* __restrict__ src, int64_t ldx, int vrows, int vcols,
-                                           double* __restrict__ dst, int dcol, double* __restrict__ R, int npad,
-                                           int cb, const double* __restrict__ Tm, double* __restrict__ Wsc,
-                                           double* __restrict__ st) {
-  constexpr int K = kSplitRows / 4;  // k-steps (registers per lane)
+                                              const double* __restrict__ src, int64_t ldx, int vrows, int vcols,
+                                              double* __restrict__ dst, int dcol, double* __restrict__ R, int npad,
+                                              int cb, const double* __restrict__ Tm, double* __restrict__ Wsc,
+                                              double* __restrict__ st) {
+  constexpr int K = kSplitRows / 4;   // W-pass k-steps (registers per lane)
+  constexpr int NRB = kSplitRows / 8;  // C-pass row blocks
+  constexpr int CB = 8;                // row blocks per C-pass batch
   const int lane = threadIdx.x & 31;
-  const uint64_t pol_ws = l2_policy_evict_last(), pol_x = l2_policy_evict_first();
+  // workspace: evict_last; X: kept for the C pass's re-read, then evict_first
+  const uint64_t pol_ws = l2_policy_evict_last(), pol_x = l2_policy_evict_first(), pol_xw = l2_policy_evict_last();
   const int frag_col = (lane >> 2) ^ ((lane & 2) << 1);
   const int vsw = ((lane >> 2) & 2) << 1;
   double* rtile = R + (int64_t)(j0 + (lane >> 2)) * npad + 8 * cb + 2 * (lane & 3);
   const double2 rinit = *reinterpret_cast<const double2*>(rtile);
-  double b[K];
-  if (kFromX) {
-    const double* bp = src + (int64_t)(lane & 3) * ldx + (lane >> 2);
-    const bool colok = (lane >> 2) < vcols;
-    const int64_t step = 4 * ldx;
-#pragma unroll
-    for (int s = 0; s < K; ++s) {
-      b[s] = (colok && 4 * s + (lane & 3) < vrows) ? ld_hint(bp, pol_x) : 0.0;
-      bp += step;
-    }
-  } else {
-    const double* bp = src + 8 * (lane & 3) + (lane >> 2);
-#pragma unroll
-    for (int s = 0; s < K; ++s) b[s] = ld_hint(bp + 32 * s, pol_ws);
-  }
+  const bool colok = !kFromX || (lane >> 2) < vcols;
   // two accumulator chains over alternating 4-row k-steps, summed (c0 + c1) + R: update_cbs's order, so a
   // tile's update is bitwise the same whichever path applies it
   double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-  const double* vslab = Bs + (lane & 3) * lds + frag_col + vj;
   double sa = 0.0, sq = 0.0;
-#pragma unroll
-  for (int s = 0; s < K; ++s) {
-    dmma(c[s & 1][0], c[s & 1][1], vslab[4 * s * lds], b[s]);
+  {
+    double b[K];
     if (kFromX) {
-      sa += fabs(b[s]);
-      sq = fma(b[s], b[s], sq);
+      const double* bp = src + (int64_t)(lane & 3) * ldx + (lane >> 2);
+      const int64_t step = 4 * ldx;
+#pragma unroll
+      for (int s = 0; s < K; ++s) {
+        b[s] = (colok && 4 * s + (lane & 3) < vrows) ? ld_hint(bp, pol_xw) : 0.0;  // re-read by the C pass
+        bp += step;
+      }
+    } else {
+      const double* bp = src + 8 * (lane & 3) + (lane >> 2);
+#pragma unroll
+      for (int s = 0; s < K; ++s) b[s] = ld_hint(bp + 32 * s, pol_ws);
+    }
+    const double* vslab = Bs + (lane & 3) * lds + frag_col + vj;
+#pragma unroll
+    for (int s = 0; s < K; ++s) {
+      dmma(c[s & 1][0], c[s & 1][1], vslab[4 * s * lds], b[s]);
+      if (kFromX) {
+        sa += fabs(b[s]);
+        sq = fma(b[s], b[s], sq);
+      }
     }
   }
   if (kFromX) {
@@ -883,26 +889,47 @@ __device__ __noinline__ void update_global(const double* __restrict__ Bs, int ld
   const double wb0 = -Wsc[(lane & 3) * 8 + (lane >> 2)];
   const double wb1 = -Wsc[(4 + (lane & 3)) * 8 + (lane >> 2)];
   __syncwarp();
-  // C tile of row block rb: element (8 rb + l/4, c) is register 2 rb + (l >> 4) of lane 4 c + (l/4) % 4
-  const int src0 = 8 * (lane & 3) + ((lane >> 2) & 3);
-  const bool hi = (lane >> 4) != 0;
+  // C pass: row block rb = rows 8 rb + l/4, cols 2 (l%4) .. +1
   const double* vrow = Bs + (lane >> 2) * lds + vj;
   const int va = (lane & 3) ^ vsw, vb = (4 + (lane & 3)) ^ vsw;
+  auto cload = [&](int rb) -> double2 {
+    const int row = 8 * rb + (lane >> 2);
+    if (kFromX) {  // zero past the last row and the last column (C layout: this lane's columns 2 (l%4), +1)
+      const int c0 = 2 * (lane & 3);
+      const double* q = src + (int64_t)row * ldx + c0;
+      const bool rok = row < vrows;
+      return make_double2(rok && c0 < vcols ? ld_hint(q, pol_x) : 0.0, rok && c0 + 1 < vcols ? ld_hint(q + 1, pol_x) : 0.0);
+    }
+    double2 v;
+    const double* q = src + 64 * rb + 8 * (lane >> 2) + 2 * (lane & 3);
+    asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(q), "l"(pol_ws));
+    return v;
+  };
+  double2 cur[CB], nxt[CB];
 #pragma unroll
-  for (int rb = 0; rb < kSplitRows / 8; ++rb) {
-    const double x0a = __shfl_sync(0xffffffffu, b[2 * rb], src0);
-    const double x0b = __shfl_sync(0xffffffffu, b[2 * rb + 1], src0);
-    const double x1a = __shfl_sync(0xffffffffu, b[2 * rb], src0 + 4);
-    const double x1b = __shfl_sync(0xffffffffu, b[2 * rb + 1], src0 + 4);
-    double cx = hi ? x0b : x0a, cy = hi ? x1b : x1a;
-    const double* vr = vrow + 8 * rb * lds;
-    dmma(cx, cy, vr[va], wb0);
-    dmma(cx, cy, vr[vb], wb1);
-    if (kToSmem)
-      *reinterpret_cast<double2*>(dst + (8 * rb + (lane >> 2)) * lds + dcol + ((2 * (lane & 3)) ^ vsw)) =
-          make_double2(cx, cy);
-    else
-      st_hint(reinterpret_cast<double2*>(dst + 64 * rb + 8 * (lane >> 2) + 2 * (lane & 3)), make_double2(cx, cy), pol_ws);
+  for (int u = 0; u < CB; ++u) cur[u] = cload(u);
+#pragma unroll
+  for (int b0 = 0; b0 < NRB; b0 += CB) {
+    if (b0 + CB < NRB) {
+#pragma unroll
+      for (int u = 0; u < CB; ++u) nxt[u] = cload(b0 + CB + u);
+    }
+#pragma unroll
+    for (int u = 0; u < CB; ++u) {
+      const int rb = b0 + u;
+      const double* vr = vrow + 8 * rb * lds;
+      double cx = cur[u].x, cy = cur[u].y;
+      dmma(cx, cy, vr[va], wb0);
+      dmma(cx, cy, vr[vb], wb1);
+      if (kToSmem)
+        *reinterpret_cast<double2*>(dst + (8 * rb + (lane >> 2)) * lds + dcol + ((2 * (lane & 3)) ^ vsw)) =
+            make_double2(cx, cy);
+      else
+        st_hint(reinterpret_cast<double2*>(dst + 64 * rb + 8 * (lane >> 2) + 2 * (lane & 3)), make_double2(cx, cy),
+                pol_ws);
+    }
+#pragma unroll
+    for (int u = 0; u < CB; ++u) cur[u] = nxt[u];
   }
 }
 
