@@ -30,7 +30,7 @@ sys.path.insert(0, ROOT)
 
 FP64_PEAK_TFLOPS = 37.0  # measured DMMA peak, profiles/r01_peaks.json (no FP64 entry in MEASURED_PEAKS.json)
 FP64_FMA_PEAK_TFLOPS = 34.2  # measured DFMA peak (same file): the narrow warp-leaf TSQR runs on the FMA pipe
-TSQR_N200_CAPTURE = "r01_tsqr_leaf_ncu_full.txt"  # ncu --set full of the n = 200 leaf, 2^21 rows
+TSQR_N200_CAPTURE = "r02_tsqr_split_leaf_ncu_full.txt"  # ncu --set full of the n = 200 (split) leaf, 2^21 rows
 METRIC = "1-pass TSQR/Gram GB/s of X and % of HBM peak at 1/2/4/8 B200 vs CPU ref"
 
 
@@ -509,6 +509,8 @@ def main():
                                         f"algorithmic {8 * n * (hi - lo)} B") if tpr else
                                        f"no committed ncu capture at n={n}",
                      "kernel": ("tsqr_warp_leaf_kernel (FP64 FMA, one Householder chain per warp)" if narrow
+                                else "tsqr_split_leaf_kernel (FP64 DMMA m8n8k4; 256-row blocks, right column "
+                                     "tiles in an L2 workspace)" if plan["block_rows"] == 256
                                 else "tsqr_leaf_kernel (FP64 DMMA m8n8k4)"),
                      "algorithmic": f"2 n^2 = {2 * n * n} flop per row x {hi - lo} rows per launch",
                      "peak_source": ("measured FP64 DFMA peak" if narrow else "measured FP64 DMMA peak")
