@@ -118,6 +118,17 @@ int tsnmf_xray_scores(const double* m, int32_t n, int64_t ldm, const double* res
 int tsnmf_xray_residual(const double* m, int32_t n, int64_t ldm, const double* a, int32_t t, int64_t lda,
                         const double* coef, int64_t ldc, double* resid, int64_t ldr, void* cuda_stream);
 
+/* ---- reduced-space steps, on the pass's small outputs without a host round trip:
+ *      scale_columns: out = a D^-1, D = diag(norms) (rows x n): reference tsqr.py:163-177 (R D^-1, the
+ *        caller rejects zero norms first, as apply_column_scaling does) and sketch.py:87-100 (G^T X D^-1);
+ *      gp_select: per row of the k x n sketch its argmin then argmax column (lowest index on ties), appended
+ *        if unseen, until r columns: reference select.py:159-178.  out[0..*count) is the selection order;
+ *        *count < r is the reference's shortfall. */
+int tsnmf_scale_columns(const double* a, int32_t rows, int32_t n, int64_t lda, const double* norms, double* out,
+                        int64_t ldo, void* cuda_stream);
+int tsnmf_gp_select(const double* sk, int32_t k, int32_t n, int64_t ldsk, int32_t r, int32_t* out, int32_t* count,
+                    void* cuda_stream);
+
 /* ---- introspection for benchmarks: chosen TSQR panel width / rows per block / CTAs per SM / leaves */
 int tsnmf_tsqr_plan(int32_t n, int64_t m, int32_t* panel, int32_t* block_rows, int32_t* ctas_per_sm,
                     int32_t* leaves);

@@ -37,6 +37,8 @@ SIGNATURES = {
     "tsnmf_sketch": (ctypes.c_int, [_vp, _i64, _i32, _i64, _i64, _u64, _i32, _vp, _i64, _vp, _i64, _vp, _sz, _vp]),
     "tsnmf_column_stats": (ctypes.c_int, [_vp, _i64, _i32, _i64, _vp, _vp, _vp, _sz, _vp]),
     "tsnmf_first_nonfinite": (ctypes.c_int, [_vp, _i64, _vp, _vp]),
+    "tsnmf_scale_columns": (ctypes.c_int, [_vp, _i32, _i32, _i64, _vp, _vp, _i64, _vp]),
+    "tsnmf_gp_select": (ctypes.c_int, [_vp, _i32, _i32, _i64, _i32, _vp, _vp, _vp]),
     "tsnmf_generate": (ctypes.c_int, [_vp, _i64, _i64, _i64, _i32, _i32, _vp, _i32, _vp, _i64, _dbl, _u64, _vp]),
     "tsnmf_nnls": (ctypes.c_int, [_vp, _i64, _i32, _i64, _vp, _i64, _i32, _dbl, _i32, _vp, _i64, _vp, _vp, _sz, _vp]),
     "tsnmf_nnls_max_cols": (ctypes.c_int, []),

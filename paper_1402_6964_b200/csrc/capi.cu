@@ -185,6 +185,22 @@ int tsnmf_nnls(const double* a, int64_t n, int32_t t, int64_t lda, const double*
 
 int tsnmf_nnls_max_cols(void) { return nnls_max_design_cols(); }
 
+int tsnmf_scale_columns(const double* a, int32_t rows, int32_t n, int64_t lda, const double* norms, double* out,
+                        int64_t ldo, void* s) {
+  if (int rc = check_matrix("scale_columns", a, rows, n, lda)) return rc;
+  if (!norms || !out || ldo < n) return set_error(kUsage, "scale_columns: bad norms / output arguments");
+  return scale_columns_run(a, rows, n, lda, norms, out, ldo, as_stream(s));
+}
+
+int tsnmf_gp_select(const double* sk, int32_t k, int32_t n, int64_t ldsk, int32_t r, int32_t* out, int32_t* count,
+                    void* s) {
+  if (int rc = check_matrix("gp_select", sk, k, n, ldsk)) return rc;
+  if (r < 1 || r > n) return set_error(kUsage, "gp_select: rank must be in 1..%d, got %d", n, r);
+  if (n > 200000) return set_error(kUsage, "gp_select: at most 200000 columns");
+  if (!out || !count) return set_error(kUsage, "gp_select: null output");
+  return gp_select_run(sk, k, n, ldsk, r, out, count, as_stream(s));
+}
+
 int tsnmf_xray_scores(const double* m, int32_t n, int64_t ldm, const double* resid, int64_t ldr,
                       const double* colnorm, double* score, void* s) {
   if (int rc = check_matrix("xray_scores", m, n, n, ldm)) return rc;

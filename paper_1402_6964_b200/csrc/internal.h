@@ -47,6 +47,10 @@ int xray_scores_run(const double* m, int n, int64_t ldm, const double* resid, in
 int xray_residual_run(const double* m, int n, int64_t ldm, const double* a, int t, int64_t lda, const double* coef,
                       int64_t ldc, double* resid, int64_t ldr, cudaStream_t st);
 
+int scale_columns_run(const double* a, int rows, int n, int64_t lda, const double* norms, double* out, int64_t ldo,
+                      cudaStream_t st);
+int gp_select_run(const double* sk, int k, int n, int64_t ldsk, int r, int* out, int* count, cudaStream_t st);
+
 int gram_max_cols();
 size_t gram_workspace_bytes(int64_t m, int n);
 int gram_run(const double* x, int64_t m, int n, int64_t ldx, double* g, int64_t ldg, double* l1, double* sumsq,

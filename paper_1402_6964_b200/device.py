@@ -93,7 +93,8 @@ def as_device_matrix(data, device=None):
     if isinstance(data, t.Tensor):
         x = data
     else:
-        x = t.from_numpy(np.ascontiguousarray(np.asarray(data, dtype=np.float64)))
+        arr = np.ascontiguousarray(np.asarray(data, dtype=np.float64))
+        x = t.from_numpy(arr if arr.flags.writeable else arr.copy())
     if x.dim() != 2:
         raise UsageError(f"chunk must be a 2-D matrix, got shape {tuple(x.shape)}")
     if x.dtype != t.float64:
@@ -253,6 +254,39 @@ def xray_residual(m, a, coef, out):
     _native.call("tsnmf_xray_residual", m.data_ptr(), n, _ld(m), a.data_ptr(), q, _ld(a), coef.data_ptr(),
                  _ld(coef), out.data_ptr(), _ld(out), stream_ptr(m.device), device=m.device, stage="xray")
     return out
+
+
+def scale_columns(a, norms):
+    """a D^-1 with D = diag(norms) (reference tsqr.py:163-177, sketch.py:87-100), on the device."""
+    t = torch()
+    a = as_device_matrix(a)
+    norms = as_device_matrix(norms.reshape(1, -1) if hasattr(norms, "reshape") else np.asarray(norms)[None, :],
+                             a.device).reshape(-1)
+    out = t.empty(a.shape, dtype=t.float64, device=a.device)
+    _native.call("tsnmf_scale_columns", a.data_ptr(), int(a.shape[0]), int(a.shape[1]), _ld(a), norms.data_ptr(),
+                 out.data_ptr(), int(out.shape[1]), stream_ptr(a.device), device=a.device, stage="scale")
+    return out
+
+
+def gp_select(sk, r: int):
+    """GP selection order on the device (reference select.py:159-178): (indices tensor, count)."""
+    t = torch()
+    sk = as_device_matrix(sk)
+    out = t.empty(int(r), dtype=t.int32, device=sk.device)
+    cnt = t.empty(1, dtype=t.int32, device=sk.device)
+    _native.call("tsnmf_gp_select", sk.data_ptr(), int(sk.shape[0]), int(sk.shape[1]), _ld(sk), int(r),
+                 out.data_ptr(), cnt.data_ptr(), stream_ptr(sk.device), device=sk.device, stage="select-gp")
+    return out, cnt
+
+
+def svd_reduced(r):
+    """Singular values and right singular vectors of the n x n factor on the device (cuSOLVER via torch: a
+    library SVD, like cuBLAS for a plain GEMM).  Row signs of V^T are LAPACK's choice on either side; every
+    consumer of the reduced matrix (SPA, XRAY, NNLS) is invariant under them."""
+    t = torch()
+    r = as_device_matrix(r)
+    _, s, vt = t.linalg.svd(r, full_matrices=False)
+    return s, vt
 
 
 # ---------------------------------------------------------------------------

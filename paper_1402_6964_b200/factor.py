@@ -167,20 +167,28 @@ class GramResult:
 # small host-side helpers that the reference also keeps on the host
 
 
-def rsvd(r: TriangularFactor) -> ReducedSVD:
-    """SVD of the n x n factor (reference tsqr.py:156-160; LAPACK on host, n x n)."""
+def rsvd(r: TriangularFactor, *, device: bool = False) -> ReducedSVD:
+    """SVD of the n x n factor (reference tsqr.py:156-160): LAPACK on the host, or (device=True) cuSOLVER on
+    the GPU (singular values to ~1e-15 relative; rows of V^T up to sign, which SPA / XRAY / NNLS ignore)."""
+    if device:
+        s, vt = dv.svd_reduced(r.entries)
+        return ReducedSVD(singular_values=s.cpu().numpy(), right_vectors=vt.cpu().numpy())
     _, s, vt = np.linalg.svd(r.entries)
     return ReducedSVD(singular_values=s, right_vectors=vt)
 
 
-def apply_column_scaling(r: TriangularFactor, stats: ColumnStats, norm_kind: str = "l1") -> TriangularFactor:
-    """R D^{-1}: the factor of the column-normalised data (reference tsqr.py:163-177)."""
+def apply_column_scaling(r: TriangularFactor, stats: ColumnStats, norm_kind: str = "l1", *,
+                         device: bool = False) -> TriangularFactor:
+    """R D^{-1}: the factor of the column-normalised data (reference tsqr.py:163-177; device=True: the
+    scaling kernel, bitwise the same quotient)."""
     norms = stats.norms(norm_kind)
     if norms.shape != (r.n,):
         raise UsageError("column stats do not match factor dimension")
     bad = np.flatnonzero(norms <= 0.0)
     if bad.size:
         raise DataError(f"column {', '.join(str(int(j)) for j in bad)} has zero norm")
+    if device:
+        return TriangularFactor(entries=dv.scale_columns(r.entries, norms).cpu().numpy())
     return TriangularFactor(entries=r.entries / norms)
 
 
