@@ -571,7 +571,7 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
                           double* __restrict__ stats_out, double* smem) {
   using L = TqLayout;
   constexpr int G = 4;  // column blocks per GEMM group
-  // W = 8: panel warp 0, helper warp 4 (both SMSP 0), six GEMM warps.  W = 4 (three CTAs per SM, n <= 64):
+  // W = 8: panel warp 0, helper warp 4 (both SMSP 0), six GEMM warps.  W = 4 (three CTAs per SM, n <= 104):
   // panel warp 0, helper warp 2, GEMM warps 1 and 3.
   constexpr int kThr = 32 * W;
   constexpr int kHelper = W == 8 ? 4 : 2;
@@ -737,7 +737,7 @@ __device__ void tsqr_fold(double* __restrict__ R, const double* __restrict__ src
   }
 }
 
-// MINB == 3 selects the 4-warp CTA (three per SM, n <= 64)
+// MINB == 3 selects the 4-warp CTA (three per SM, n <= 104)
 template <int MINB>
 constexpr int tq_warps() { return MINB == 3 ? 4 : kTqWarps; }
 
@@ -1612,10 +1612,11 @@ bool tq_config(int n, TqChoice* out) {
   // DESIGN.md).  Narrow matrices (n <= 64) fit a full 128-row block in half the shared memory, so two CTAs
   // per SM give two independent panel chains (measured +50% at n = 25 and 64); wider ones run one CTA
   // with the largest block.  TSNMF_TSQR_CTAS=1/2/3 overrides for tuning.
-  // n <= 96: three 4-warp CTAs per SM (three panel chains, 64-112-row blocks, 168 registers): measured
+  // n <= 104: three 4-warp CTAs per SM (three panel chains, 64-112-row blocks, 168 registers): measured
   // n=48 370 -> 476, n=64 355 -> 406 (vs two 8-warp CTAs, whose 128-register cap forces spills), n=72
   // 273 -> 388, n=96 272 -> 328 GB/s (vs one 8-warp CTA); n=128 is better with one CTA (270 vs 237)
-  int minb = n <= 104 ? 3 : 1;  // (97..104 have n = 96's padded width and shared-memory footprint)
+  // (97..104: npad = 104, but the block stride lds (104) and rows (64) match n = 96's, so the same fit)
+  int minb = n <= 104 ? 3 : 1;
   if (const char* e = getenv("TSNMF_TSQR_CTAS")) minb = atoi(e) == 3 ? 3 : (atoi(e) == 2 ? 2 : 1);
   if (minb == 3 && n <= 128 && tq_choose(n, 3, out) && out->g.brows >= 48) return true;
   if (minb >= 2 && tq_choose(n, 2, out) && out->g.brows >= (n <= 64 ? 128 : 48)) return true;

@@ -131,7 +131,8 @@ def test_device_chunk_batching(oracle):
     assert rel_err(res.sketch.entries, whole.sketch.entries) <= 1e-12
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 9, 15, 16, 17, 25, 31, 33, 64, 100, 127, 200, 255, 256, 300, 512])
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 9, 15, 16, 17, 25, 31, 33, 64, 72, 97, 100, 104, 105, 127, 160, 200,
+                               208, 209, 255, 256, 300, 512])
 def test_factor_matches_oracle_many_widths(oracle, n):
     rng = np.random.default_rng(n)
     m = max(3 * n, 50) + 13
@@ -407,3 +408,21 @@ def test_column_stats_every_block_size(m, n):
     _, l1, sq = dv.tsqr(dev(x))
     np.testing.assert_allclose(l1.cpu().numpy(), np.abs(x).sum(0), rtol=1e-12)
     np.testing.assert_allclose(sq.cpu().numpy(), (x * x).sum(0), rtol=1e-12)
+
+
+@pytest.mark.parametrize("n,m", [(105, 70_001), (128, 131_075), (160, 99_999), (200, 300_001), (208, 65_537)])
+def test_split_leaf_many_blocks(oracle, n, m):
+    """The split leaf (105 <= n <= 208: 256-row blocks, right column tiles in an L2 workspace, moved into shared
+    slots as the left tiles die) over many blocks per leaf and a ragged last block, strided X; R against the
+    oracle, the fused column stats, and bitwise repeatability."""
+    rng = np.random.default_rng(n + m)
+    xs = rng.uniform(-1, 1, (m, n + 3)) * np.logspace(0, -3, n + 3)
+    x = dv.torch().from_numpy(xs).cuda()[:, 1:n + 1]
+    assert dv.tsqr_plan(n, m)["block_rows"] == 256
+    r, l1, sq = dv.tsqr(x)
+    xh = xs[:, 1:n + 1]
+    want = oracle.factor_chunk(xh)
+    assert rel_err(r.cpu().numpy(), want) <= R_TOL
+    np.testing.assert_allclose(l1.cpu().numpy(), np.abs(xh).sum(0), rtol=1e-12)
+    np.testing.assert_allclose(sq.cpu().numpy(), (xh * xh).sum(0), rtol=1e-12)
+    assert np.array_equal(r.cpu().numpy(), dv.tsqr(x)[0].cpu().numpy())

@@ -222,3 +222,16 @@ def test_default_sketch_rows():
     from paper_1402_6964_b200.projection import default_sketch_rows
 
     assert [default_sketch_rows(r) for r in (1, 2, 3, 10, 20, 64)] == [2, 3, 7, 47, 120, 533]
+
+
+def test_pack_pieces_parallel_matches_vstack(monkeypatch):
+    """Host chunks are packed into the pinned staging buffer by several threads (factor._pack_pieces)."""
+    from paper_1402_6964_b200 import factor as f
+
+    monkeypatch.setattr(f, "_PACK_MIN_BYTES", 0)
+    g = np.random.default_rng(1)
+    for sizes in ([1], [3, 7, 8192, 100, 1, 4000], [5] * 37, [100_000, 3]):
+        arrs = [g.standard_normal((r, 9)) for r in sizes]
+        dst = np.zeros((sum(sizes) + 5, 9))
+        f._pack_pieces(dst, arrs)
+        assert np.array_equal(dst[:sum(sizes)], np.vstack(arrs)) and not dst[sum(sizes):].any()
