@@ -181,6 +181,181 @@ __global__ void gram_reduce_kernel(const double* __restrict__ partial, int64_t s
   }
 }
 
+// ---------------------------------------------------------------------------
+// Narrow Gram (n <= 32, e.g. config C4 n = 25): HBM-bound (3.25 flop/B at n = 25), so no shared
+// memory staging at all.  Both DMMA operands of a 4-row k-step are the same fragment X[i + l%4][8T + l/4]
+// (tile column T), so each lane loads its fragments straight from global memory (TC 8-byte loads per
+// k-step, U k-steps per group in flight, the next group's loads issued before the current group's DMMAs)
+// and every warp accumulates the whole upper triangle (TC (TC + 1) / 2 tiles) in registers.  A width of the
+// form 8 TC + 1 (25 = 24 + 1) keeps its last column off the tensor pipe: padding it to a fourth tile column
+// would add 4 DMMAs per k-step (10 instead of 6) for 25 useful products, so its 8 TC + 1 dot products are
+// plain FMAs against the fragments already in registers (RT = 1).  Column l1 comes from the fragments,
+// sum of squares = diag G.  Warps take row groups round-robin; warp partials are summed in warp order
+// through shared memory, CTA partials in CTA order by gram_narrow_reduce_kernel (deterministic).
+// 33 <= n <= 64 (config C5) runs the same kernel with 15..36 accumulator tiles per warp (one CTA per SM, up to
+// 255 registers; FP64-bound there, 36 DMMAs per k-step at n = 64).
+constexpr int kGnWarps = 8;      // per CTA; two CTAs per SM up to four tile columns, one above
+constexpr int kGnTailMax = 72;   // tail-column partials: 8 TC dots + self, padded
+constexpr int kGnL1Max = 72;     // column l1 partials (<= 64 columns), padded
+constexpr int kGnMaxCols = 64;
+
+__host__ __device__ constexpr int gn_tiles(int tc) { return tc * (tc + 1) / 2; }
+// k-steps per row group: <= 16 fragment loads in flight per lane (cols = TC + RT)
+__host__ __device__ constexpr int gn_unroll(int cols) { return cols >= 5 ? 2 : (cols >= 3 ? 4 : (cols == 2 ? 8 : 16)); }
+__host__ __device__ constexpr int gn_partial_stride(int tc) { return gn_tiles(tc) * 64 + kGnTailMax + kGnL1Max; }
+
+template <int TC, int RT>
+__global__ void __launch_bounds__(32 * kGnWarps, TC <= 4 ? 2 : 1)
+    gram_narrow_kernel(const double* __restrict__ x, int64_t m, int64_t ldx, int n, int64_t rows_per_cta,
+                       double* __restrict__ partial) {
+  constexpr int NT = gn_tiles(TC);
+  constexpr int U = gn_unroll(TC + RT);
+  constexpr int PS = gn_partial_stride(TC);
+  __shared__ double sred[PS];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kr = lane & 3, cj = lane >> 2;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t r1 = min64(m, r0 + rows_per_cta);
+  const int ct = 8 * TC;  // tail column (RT = 1)
+  bool colok[TC];
+#pragma unroll
+  for (int T = 0; T < TC; ++T) colok[T] = 8 * T + cj < (RT ? ct : n);
+
+  double acc[NT][2];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
+  double sa[TC], tacc[TC];
+#pragma unroll
+  for (int T = 0; T < TC; ++T) sa[T] = tacc[T] = 0.0;
+  double tself = 0.0, tl1 = 0.0;
+
+  double cur[U][TC + RT], nxt[U][TC + RT];
+  auto load = [&](double (&f)[U][TC + RT], int64_t g0) {  // rows g0 .. g0 + 4U of the CTA's range
+    const double* p = x + (g0 + kr) * ldx + cj;
+    if (g0 + 4 * U <= r1) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+#pragma unroll
+        for (int T = 0; T < TC; ++T) f[u][T] = colok[T] ? __ldg(p + 8 * T) : 0.0;
+        if (RT) f[u][TC] = __ldg(p + ct - cj);
+        p += 4 * ldx;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool rok = g0 + 4 * u + kr < r1;
+#pragma unroll
+        for (int T = 0; T < TC; ++T) f[u][T] = (rok && colok[T]) ? __ldg(p + 8 * T) : 0.0;
+        if (RT) f[u][TC] = rok ? __ldg(p + ct - cj) : 0.0;
+        p += 4 * ldx;
+      }
+    }
+  };
+  const int64_t gstep = (int64_t)4 * U * kGnWarps;
+  int64_t g0 = r0 + (int64_t)4 * U * warp;
+  if (g0 < r1) load(cur, g0);
+  while (g0 < r1) {
+    const int64_t gn = g0 + gstep;
+    if (gn < r1) load(nxt, gn);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      int t = 0;
+#pragma unroll
+      for (int I = 0; I < TC; ++I)
+#pragma unroll
+        for (int J = I; J < TC; ++J) {
+          dmma(acc[t][0], acc[t][1], cur[u][I], cur[u][J]);
+          ++t;
+        }
+#pragma unroll
+      for (int T = 0; T < TC; ++T) sa[T] += fabs(cur[u][T]);
+      if (RT) {
+        const double xt = cur[u][TC];
+#pragma unroll
+        for (int T = 0; T < TC; ++T) tacc[T] = fma(cur[u][T], xt, tacc[T]);
+        tself = fma(xt, xt, tself);
+        tl1 += fabs(xt);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int T = 0; T < TC + RT; ++T) cur[u][T] = nxt[u][T];
+    g0 = gn;
+  }
+  // sums over the four k-rows of a lane group (fixed order)
+#pragma unroll
+  for (int T = 0; T < TC; ++T) {
+    sa[T] += __shfl_xor_sync(0xffffffffu, sa[T], 1);
+    sa[T] += __shfl_xor_sync(0xffffffffu, sa[T], 2);
+    if (RT) {
+      tacc[T] += __shfl_xor_sync(0xffffffffu, tacc[T], 1);
+      tacc[T] += __shfl_xor_sync(0xffffffffu, tacc[T], 2);
+    }
+  }
+  if (RT) {
+    tself += __shfl_xor_sync(0xffffffffu, tself, 1);
+    tself += __shfl_xor_sync(0xffffffffu, tself, 2);
+    tl1 += __shfl_xor_sync(0xffffffffu, tl1, 1);
+    tl1 += __shfl_xor_sync(0xffffffffu, tl1, 2);
+  }
+  // warp partials -> CTA partial, in warp order
+  for (int i = tid; i < PS; i += 32 * kGnWarps) sred[i] = 0.0;
+  __syncthreads();
+  for (int w = 0; w < kGnWarps; ++w) {
+    if (warp == w) {
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        sred[t * 64 + 2 * lane] += acc[t][0];
+        sred[t * 64 + 2 * lane + 1] += acc[t][1];
+      }
+      if (kr == 0) {
+#pragma unroll
+        for (int T = 0; T < TC; ++T) {
+          sred[NT * 64 + kGnTailMax + 8 * T + cj] += sa[T];
+          if (RT) sred[NT * 64 + 8 * T + cj] += tacc[T];
+        }
+      }
+      if (RT && lane == 0) {
+        sred[NT * 64 + ct] += tself;
+        sred[NT * 64 + kGnTailMax + ct] += tl1;
+      }
+    }
+    __syncthreads();
+  }
+  double* dst = partial + (int64_t)blockIdx.x * PS;
+  for (int i = tid; i < PS; i += 32 * kGnWarps) dst[i] = sred[i];
+}
+
+// G(i, j), i <= j, summed over the CTA partials in CTA order; mirrored; sumsq = diag; l1.
+__global__ void gram_narrow_reduce_kernel(const double* __restrict__ partial, int ctas, int tc, int rt, int n,
+                                          double* __restrict__ out, int64_t ldg, double* __restrict__ l1,
+                                          double* __restrict__ sumsq) {
+  const int nt = gn_tiles(tc), ps = gn_partial_stride(tc), ct = 8 * tc;
+  const int i = blockIdx.x;
+  for (int j = i + threadIdx.x; j <= n; j += blockDim.x) {
+    int off;
+    if (j == n) {  // column l1 of column i
+      if (!l1) continue;
+      off = nt * 64 + kGnTailMax + i;
+    } else if (rt && j == ct) {
+      off = nt * 64 + i;  // i < ct: dot with the tail column; i == ct: its own square sum
+    } else {
+      const int I = i >> 3, J = j >> 3;
+      off = (I * tc - I * (I - 1) / 2 + (J - I)) * 64 + (i & 7) * 8 + (j & 7);
+    }
+    double acc = 0.0;
+    for (int c = 0; c < ctas; ++c) acc += partial[(int64_t)c * ps + off];
+    if (j == n) {
+      l1[i] = acc;
+    } else {
+      out[(int64_t)i * ldg + j] = acc;
+      out[(int64_t)j * ldg + i] = acc;
+      if (i == j && sumsq) sumsq[i] = acc;
+    }
+  }
+}
+
 __global__ void l1_reduce_kernel(const double* __restrict__ l1part, int64_t splits, int stride, int n,
                                  double* __restrict__ l1) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -242,12 +417,72 @@ int sm_count() {
   return sms;
 }
 
+// Narrow path (n <= 64): TSNMF_GRAM_NARROW=0 selects the staged kernel, TSNMF_GRAM_TAIL=0 pads a width of
+// the form 8 TC + 1 to another tile column instead of the FMA tail.
+bool gn_path(int n) {
+  if (n > kGnMaxCols) return false;
+  if (const char* e = getenv("TSNMF_GRAM_NARROW")) return atoi(e) != 0;
+  return true;
+}
+struct GnPlan {
+  int tc, rt, ctas;
+  int64_t rpc;
+};
+GnPlan gn_plan(int64_t m, int n, int sms) {
+  GnPlan p;
+  p.rt = (n == 17 || n == 25) ? 1 : 0;  // measured: n = 25 6113 vs 4353 GB/s padded, n = 17 5924 vs 5109; n = 9 loses (4411 vs 5178)
+  if (const char* e = getenv("TSNMF_GRAM_TAIL")) p.rt = p.rt && atoi(e) != 0;
+  p.tc = p.rt ? n / 8 : (int)ceil_div(n, 8);
+  const int64_t grp = 4 * gn_unroll(p.tc + p.rt);
+  const int64_t ctas = max64(1, min64((int64_t)(p.tc <= 4 ? 2 : 1) * sms, ceil_div(m, grp * kGnWarps)));
+  p.rpc = round_up(ceil_div(m, ctas), grp);
+  p.ctas = (int)max64(1, ceil_div(m, p.rpc));
+  return p;
+}
+size_t gn_ws_doubles(const GnPlan& p) { return (size_t)p.ctas * gn_partial_stride(p.tc); }
+
+template <int TC, int RT>
+int gn_launch(const double* x, int64_t m, int64_t ldx, int n, const GnPlan& p, double* partial, cudaStream_t st) {
+  gram_narrow_kernel<TC, RT><<<p.ctas, 32 * kGnWarps, 0, st>>>(x, m, ldx, n, p.rpc, partial);
+  TSNMF_LAUNCH_CHECK();
+  return kOk;
+}
+
+int gn_run(const double* x, int64_t m, int n, int64_t ldx, double* gout, int64_t ldg, double* l1, double* sumsq,
+           void* ws, size_t ws_bytes, cudaStream_t st) {
+  const GnPlan p = gn_plan(m, n, sm_count());
+  const size_t need = sizeof(double) * gn_ws_doubles(p);
+  if (ws_bytes < need) return set_error(kUsage, "gram: workspace too small (%zu < %zu bytes)", ws_bytes, need);
+  double* partial = reinterpret_cast<double*>(ws);
+  prof_mark(kProfGram, true, st);
+  int rc;
+  switch (p.tc * 2 + p.rt) {
+    case 2: rc = gn_launch<1, 0>(x, m, ldx, n, p, partial, st); break;
+    case 3: rc = gn_launch<1, 1>(x, m, ldx, n, p, partial, st); break;
+    case 4: rc = gn_launch<2, 0>(x, m, ldx, n, p, partial, st); break;
+    case 5: rc = gn_launch<2, 1>(x, m, ldx, n, p, partial, st); break;
+    case 6: rc = gn_launch<3, 0>(x, m, ldx, n, p, partial, st); break;
+    case 7: rc = gn_launch<3, 1>(x, m, ldx, n, p, partial, st); break;
+    case 8: rc = gn_launch<4, 0>(x, m, ldx, n, p, partial, st); break;
+    case 10: rc = gn_launch<5, 0>(x, m, ldx, n, p, partial, st); break;
+    case 12: rc = gn_launch<6, 0>(x, m, ldx, n, p, partial, st); break;
+    case 14: rc = gn_launch<7, 0>(x, m, ldx, n, p, partial, st); break;
+    default: rc = gn_launch<8, 0>(x, m, ldx, n, p, partial, st); break;
+  }
+  if (rc) return rc;
+  prof_mark(kProfGram, false, st);
+  gram_narrow_reduce_kernel<<<n, 64, 0, st>>>(partial, p.ctas, p.tc, p.rt, n, gout, ldg, l1, sumsq);
+  TSNMF_LAUNCH_CHECK();
+  return kOk;
+}
+
 }  // namespace
 
 int gram_max_cols() { return 512; }
 
 size_t gram_workspace_bytes(int64_t m, int n) {
   if (n < 1 || n > gram_max_cols()) return 0;
+  if (gn_path(n)) return sizeof(double) * gn_ws_doubles(gn_plan(max64(m, 1), n, sm_count())) + 256;
   GrGeom g = gr_geom(max64(m, 1), n, sm_count());
   const int64_t splits = gr_splits(max64(m, 1), g);
   return sizeof(double) * (size_t)(splits * g.ks * g.nst * 256 + splits * g.npad) + 256;
@@ -270,6 +505,7 @@ int gram_launch(const double* x, int64_t m, int64_t ldx, const GrGeom& g, double
 int gram_run(const double* x, int64_t m, int n, int64_t ldx, double* gout, int64_t ldg, double* l1, double* sumsq,
              void* ws, size_t ws_bytes, cudaStream_t st) {
   if (n > gram_max_cols()) return set_error(kUsage, "gram: n = %d exceeds %d", n, gram_max_cols());
+  if (gn_path(n)) return gn_run(x, m, n, ldx, gout, ldg, l1, sumsq, ws, ws_bytes, st);
   GrGeom g = gr_geom(m, n, sm_count());
   const int64_t splits = gr_splits(m, g);
   const size_t need = sizeof(double) * (size_t)(splits * g.ks * g.nst * 256 + splits * g.npad);

@@ -306,6 +306,31 @@ def test_gram_matches_numpy(n):
     np.testing.assert_allclose(g.stats.l2, np.linalg.norm(x, axis=0), rtol=1e-12)
 
 
+@pytest.mark.parametrize("n", list(range(1, 65)))
+def test_gram_narrow_every_width(n, monkeypatch):
+    """Narrow Gram kernel (n <= 64: fragments straight from global memory, FMA tail column at n = 17, 25):
+    ragged row counts (below one k-step, below one row group, many CTAs), a strided view, and the
+    padded-tile / staged variants, all against numpy."""
+    rng = np.random.default_rng(100 + n)
+    for m in (1, 3, 18, 1023, 70_001):
+        x = rng.standard_normal((m, n)) * np.logspace(0, -2, n)
+        g, l1, sq = dv.gram(dev(x))
+        assert rel_err(g.cpu().numpy(), x.T @ x) <= 1e-13, (n, m)
+        assert np.array_equal(g.cpu().numpy(), g.cpu().numpy().T)
+        np.testing.assert_allclose(l1.cpu().numpy(), np.abs(x).sum(0), rtol=1e-12)
+        np.testing.assert_allclose(sq.cpu().numpy(), (x * x).sum(0), rtol=1e-12)
+    wide = rng.standard_normal((4099, 72))
+    view = dev(wide)[:, 5:5 + n]
+    want = wide[:, 5:5 + n].T @ wide[:, 5:5 + n]
+    base = dv.gram(view)[0].cpu().numpy()
+    assert rel_err(base, want) <= 1e-13
+    assert np.array_equal(base, dv.gram(view)[0].cpu().numpy())  # fixed-order sums: bitwise repeatable
+    for var in ("TSNMF_GRAM_TAIL", "TSNMF_GRAM_NARROW"):
+        monkeypatch.setenv(var, "0")
+        assert rel_err(dv.gram(view)[0].cpu().numpy(), want) <= 1e-13, var
+        monkeypatch.delenv(var)
+
+
 def test_gram_equivalence_invariant():
     """‖RᵀR − XᵀX‖_F ≤ 1e-10 ‖XᵀX‖_F (reference SPEC.md:164) on the device outputs."""
     x = np.random.default_rng(11).uniform(0, 1, (100_000, 50))
