@@ -356,6 +356,168 @@ __global__ void gram_narrow_reduce_kernel(const double* __restrict__ partial, in
   }
 }
 
+// ---------------------------------------------------------------------------
+// Cyclic register Gram for TC = W RPW + 1 tile columns with W warps per CTA (W = 12, RPW = 2: config C2,
+// n = 193..200, 25 tile columns).  With an odd number of tile columns every unordered pair {I, J} is covered
+// exactly once by the tiles (I, (I + d) mod TC), d = 0..(TC - 1) / 2, so the upper triangle is TC "tile
+// rows" of D = (TC + 1) / 2 tiles each and no tile is computed twice.  Warp w owns tile rows RPW w .. RPW w +
+// RPW - 1: its accumulators (RPW D tiles) stay in registers for the whole pass, its operands are the
+// RPW + D - 1 fragments of tile columns RPW w .. (mod TC), loaded straight from global memory (all warps of
+// the CTA walk the same rows, so after the first toucher they are L1 / L2 hits; an L2 prefetch runs kGcAhead
+// k-steps ahead), A = f[r], B = f[r + d]: static register indices.  The leftover tile row TC - 1 is shared
+// out: warps 0 .. W/2 - 1 take RPW of its tiles each (one more fragment, tile column TC - 1), warp W/2's
+// extra slot holds the last diagonal tile; the other warps' extra slots repeat it (uniform code: every warp
+// issues RPW (D + 1) DMMAs per k-step for RPW + D loads).  DMMA slots per k-step at n = 200: 336 for 314
+// useful (93%; the staged kernel's 16 x 16 super-tiles: 384).
+#ifndef TSNMF_GC_L1PF
+#define TSNMF_GC_L1PF 0
+#endif
+constexpr int kGcAhead = 8;  // L2 prefetch distance in k-steps (4 rows each)
+
+template <int W, int RPW>
+struct GcShape {
+  static constexpr int TC = W * RPW + 1;
+  static constexpr int D = (TC + 1) / 2;
+  static constexpr int NF = RPW + D - 1;        // fragments of the warp's own tile rows
+  static constexpr int NT = RPW * D + RPW;      // accumulator tiles per warp (own rows + extra slots)
+  static constexpr int PS = W * NT * 64 + 8 * TC;  // per-CTA partial: tiles, then column l1
+};
+
+template <int W, int RPW, bool kFullCols>
+__global__ void __launch_bounds__(32 * W, 1)
+    gram_cyclic_kernel(const double* __restrict__ x, int64_t m, int64_t ldx, int n, int64_t rows_per_cta,
+                       double* __restrict__ partial) {
+  using S = GcShape<W, RPW>;
+  constexpr int TC = S::TC, D = S::D, NF = S::NF;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kr = lane & 3, cj = lane >> 2;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t r1 = min64(m, r0 + rows_per_cta);
+  // fragment q <-> tile column (RPW warp + q) mod TC; fragment NF <-> tile column TC - 1.  Addressed from one
+  // running row pointer p (this lane's row of the k-step, at the warp's first tile column): p[off(q)]
+  const int qwrap = TC - RPW * warp;  // fragments q >= qwrap wrap around to tile column q - qwrap
+  auto off = [&](int q) { return q == NF ? 8 * (qwrap - 1) : (q < qwrap ? 8 * q : 8 * (q - TC)); };
+  auto colok = [&](int q) { return kFullCols || 8 * RPW * warp + cj + off(q) < n; };
+  const bool low = warp < W / 2;  // extra slots: (TC - 1, RPW warp + e) for the low warps, the last diagonal tile otherwise
+  double acc[RPW][D][2], ext[RPW][2];
+#pragma unroll
+  for (int r = 0; r < RPW; ++r) {
+    ext[r][0] = ext[r][1] = 0.0;
+#pragma unroll
+    for (int d = 0; d < D; ++d) acc[r][d][0] = acc[r][d][1] = 0.0;
+  }
+  double sa[RPW + 1];
+#pragma unroll
+  for (int r = 0; r <= RPW; ++r) sa[r] = 0.0;
+  // L2 prefetch: 4 rows x ceil(8 n / 128) lines per k-step, kGcAhead k-steps ahead
+  const int lines = (8 * n + 127) / 128 + 1;
+  const int pf_row = tid / lines, pf_line = tid - pf_row * lines;
+  const bool pf_on = pf_row < 4 && 128 * pf_line < 8 * n;
+  const char* pf = reinterpret_cast<const char*>(x + (r0 + 4 * kGcAhead + pf_row) * ldx) + 128 * pf_line;
+  int64_t pf_left = r1 - (r0 + 4 * kGcAhead + pf_row);  // rows from the prefetched row to the end of the range
+
+  const double* p = x + (r0 + kr) * ldx + 8 * RPW * warp + cj;
+  const int64_t pstep = 4 * ldx;
+  // all loads of a k-step, then all its DMMAs (loads reissued one by one behind the DMMAs that free their
+  // registers measured slower, 1019 vs 1106 GB/s with 8 warps: the partner warps' turns hide the wait)
+  auto kstep = [&](const double (&f)[NF + 1]) {
+#pragma unroll
+    for (int r = 0; r < RPW; ++r)
+#pragma unroll
+      for (int d = 0; d < D; ++d) dmma(acc[r][d][0], acc[r][d][1], f[r], f[r + d]);
+#pragma unroll
+    for (int e = 0; e < RPW; ++e) {
+      const double b = low ? f[e] : f[NF];
+      dmma(ext[e][0], ext[e][1], f[NF], b);
+    }
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) sa[r] += fabs(f[r]);
+    sa[RPW] += fabs(f[NF]);
+  };
+  int64_t g0 = r0;
+  for (; g0 + 4 <= r1; g0 += 4) {
+    if (pf_on && pf_left > 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(pf));
+    pf += 32 * ldx;
+    pf_left -= 4;
+    double f[NF + 1];
+#pragma unroll
+    for (int q = 0; q <= NF; ++q) f[q] = colok(q) ? __ldg(p + off(q)) : 0.0;
+    p += pstep;
+#if TSNMF_GC_L1PF
+    if (g0 + 8 <= r1) {
+#pragma unroll
+      for (int q = 0; q <= NF; ++q)
+        if (colok(q)) asm volatile("prefetch.global.L1 [%0];" ::"l"(p + off(q)));
+    }
+#endif
+    kstep(f);
+  }
+  if (g0 < r1) {  // last, partial k-step of the range
+    const bool rok = g0 + kr < r1;
+    double f[NF + 1];
+#pragma unroll
+    for (int q = 0; q <= NF; ++q) f[q] = (rok && colok(q)) ? __ldg(p + off(q)) : 0.0;
+    kstep(f);
+  }
+  double* dst = partial + (int64_t)blockIdx.x * S::PS + (int64_t)warp * S::NT * 64;
+#pragma unroll
+  for (int r = 0; r < RPW; ++r)
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+      *reinterpret_cast<double2*>(dst + (r * D + d) * 64 + 2 * lane) = make_double2(acc[r][d][0], acc[r][d][1]);
+#pragma unroll
+  for (int e = 0; e < RPW; ++e)
+    *reinterpret_cast<double2*>(dst + (RPW * D + e) * 64 + 2 * lane) = make_double2(ext[e][0], ext[e][1]);
+  // column l1: sum over the four k-rows of a lane group; warp w owns tile columns RPW w .. + RPW - 1, warp 0
+  // also the last one
+  double* l1dst = partial + (int64_t)blockIdx.x * S::PS + (int64_t)W * S::NT * 64;
+#pragma unroll
+  for (int r = 0; r <= RPW; ++r) {
+    sa[r] += __shfl_xor_sync(0xffffffffu, sa[r], 1);
+    sa[r] += __shfl_xor_sync(0xffffffffu, sa[r], 2);
+    if (kr == 0 && (r < RPW || warp == 0)) l1dst[8 * (r < RPW ? RPW * warp + r : TC - 1) + cj] = sa[r];
+  }
+}
+
+// G(i, j), i <= j, from the owner's tile (see gram_cyclic_kernel), summed over the CTA partials in CTA order
+template <int W, int RPW>
+__global__ void gram_cyclic_reduce_kernel(const double* __restrict__ partial, int ctas, int n,
+                                          double* __restrict__ out, int64_t ldg, double* __restrict__ l1,
+                                          double* __restrict__ sumsq) {
+  using S = GcShape<W, RPW>;
+  constexpr int TC = S::TC, D = S::D;
+  const int i = blockIdx.x;
+  for (int j = i + threadIdx.x; j <= n; j += blockDim.x) {
+    int off;
+    if (j == n) {
+      if (!l1) continue;
+      off = W * S::NT * 64 + i;
+    } else {
+      const int ti = i >> 3, tj = j >> 3, d = tj - ti;
+      int w, slot, er, ec;  // owner warp, tile slot, element (row, col)
+      if (ti == TC - 1) {  // last diagonal tile: warp W/2's extra slot 0
+        w = W / 2, slot = RPW * D, er = i & 7, ec = j & 7;
+      } else if (d < D) {  // tile (ti, tj) in tile row ti
+        w = ti / RPW, slot = (ti % RPW) * D + d, er = i & 7, ec = j & 7;
+      } else if (tj == TC - 1) {  // tile (TC - 1, ti) of the leftover row: warp ti / RPW's extra slot
+        w = ti / RPW, slot = RPW * D + ti % RPW, er = j & 7, ec = i & 7;
+      } else {  // tile (tj, ti) in tile row tj (wrapped), transposed
+        w = tj / RPW, slot = (tj % RPW) * D + (TC - d), er = j & 7, ec = i & 7;
+      }
+      off = (w * S::NT + slot) * 64 + er * 8 + ec;
+    }
+    double acc = 0.0;
+    for (int c = 0; c < ctas; ++c) acc += partial[(int64_t)c * S::PS + off];
+    if (j == n) {
+      l1[i] = acc;
+    } else {
+      out[(int64_t)i * ldg + j] = acc;
+      out[(int64_t)j * ldg + i] = acc;
+      if (i == j && sumsq) sumsq[i] = acc;
+    }
+  }
+}
+
 __global__ void l1_reduce_kernel(const double* __restrict__ l1part, int64_t splits, int stride, int n,
                                  double* __restrict__ l1) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -476,6 +638,60 @@ int gn_run(const double* x, int64_t m, int n, int64_t ldx, double* gout, int64_t
   return kOk;
 }
 
+// Cyclic register Gram: n = 193..200 (25 tile columns); TSNMF_GRAM_CYCLIC=0 selects the staged kernel.
+bool gc_path(int n) {
+  if (n <= 192 || n > 200) return false;
+  if (const char* e = getenv("TSNMF_GRAM_CYCLIC")) return atoi(e) != 0;
+  return true;
+}
+struct GcPlan {
+  int ctas;
+  int64_t rpc;
+};
+GcPlan gc_plan(int64_t m, int sms) {
+  GcPlan p;
+  const int64_t ctas = max64(1, min64(sms, ceil_div(m, 256)));
+  p.rpc = round_up(ceil_div(m, ctas), 4);
+  p.ctas = (int)max64(1, ceil_div(m, p.rpc));
+  return p;
+}
+template <int W, int RPW>
+int gc_launch(const double* x, int64_t m, int n, int64_t ldx, double* gout, int64_t ldg, double* l1, double* sumsq,
+              void* ws, size_t ws_bytes, cudaStream_t st) {
+  using S = GcShape<W, RPW>;
+  const GcPlan p = gc_plan(m, sm_count());
+  const size_t need = sizeof(double) * (size_t)p.ctas * S::PS;
+  if (ws_bytes < need) return set_error(kUsage, "gram: workspace too small (%zu < %zu bytes)", ws_bytes, need);
+  double* partial = reinterpret_cast<double*>(ws);
+  prof_mark(kProfGram, true, st);
+  if (n == 8 * S::TC)
+    gram_cyclic_kernel<W, RPW, true><<<p.ctas, 32 * W, 0, st>>>(x, m, ldx, n, p.rpc, partial);
+  else
+    gram_cyclic_kernel<W, RPW, false><<<p.ctas, 32 * W, 0, st>>>(x, m, ldx, n, p.rpc, partial);
+  TSNMF_LAUNCH_CHECK();
+  prof_mark(kProfGram, false, st);
+  gram_cyclic_reduce_kernel<W, RPW><<<n, 128, 0, st>>>(partial, p.ctas, n, gout, ldg, l1, sumsq);
+  TSNMF_LAUNCH_CHECK();
+  return kOk;
+}
+// 25 tile columns: 8 warps x 3 tile rows at n = 200 (no column predicates; 1161 vs 974 GB/s with 12 warps), 12
+// warps x 2 tile rows for the ragged widths 193..199 (996 vs 882 GB/s); TSNMF_GRAM_CYCLIC=8 / 12 forces one.
+bool gc_eight(int n) {
+  if (const char* e = getenv("TSNMF_GRAM_CYCLIC")) {
+    if (atoi(e) == 8) return true;
+    if (atoi(e) == 12) return false;
+  }
+  return n == 200;
+}
+size_t gc_ws_doubles(int64_t m, int n) {
+  return (size_t)gc_plan(m, sm_count()).ctas * (gc_eight(n) ? GcShape<8, 3>::PS : GcShape<12, 2>::PS);
+}
+int gc_run(const double* x, int64_t m, int n, int64_t ldx, double* gout, int64_t ldg, double* l1, double* sumsq,
+           void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (gc_eight(n)) return gc_launch<8, 3>(x, m, n, ldx, gout, ldg, l1, sumsq, ws, ws_bytes, st);
+  return gc_launch<12, 2>(x, m, n, ldx, gout, ldg, l1, sumsq, ws, ws_bytes, st);
+}
+
 }  // namespace
 
 int gram_max_cols() { return 512; }
@@ -483,6 +699,7 @@ int gram_max_cols() { return 512; }
 size_t gram_workspace_bytes(int64_t m, int n) {
   if (n < 1 || n > gram_max_cols()) return 0;
   if (gn_path(n)) return sizeof(double) * gn_ws_doubles(gn_plan(max64(m, 1), n, sm_count())) + 256;
+  if (gc_path(n)) return sizeof(double) * gc_ws_doubles(max64(m, 1), n) + 256;
   GrGeom g = gr_geom(max64(m, 1), n, sm_count());
   const int64_t splits = gr_splits(max64(m, 1), g);
   return sizeof(double) * (size_t)(splits * g.ks * g.nst * 256 + splits * g.npad) + 256;
@@ -506,6 +723,7 @@ int gram_run(const double* x, int64_t m, int n, int64_t ldx, double* gout, int64
              void* ws, size_t ws_bytes, cudaStream_t st) {
   if (n > gram_max_cols()) return set_error(kUsage, "gram: n = %d exceeds %d", n, gram_max_cols());
   if (gn_path(n)) return gn_run(x, m, n, ldx, gout, ldg, l1, sumsq, ws, ws_bytes, st);
+  if (gc_path(n)) return gc_run(x, m, n, ldx, gout, ldg, l1, sumsq, ws, ws_bytes, st);
   GrGeom g = gr_geom(m, n, sm_count());
   const int64_t splits = gr_splits(m, g);
   const size_t need = sizeof(double) * (size_t)(splits * g.ks * g.nst * 256 + splits * g.npad);
