@@ -370,7 +370,7 @@ __global__ void gram_narrow_reduce_kernel(const double* __restrict__ partial, in
 // issues RPW (D + 1) DMMAs per k-step for RPW + D loads).  DMMA slots per k-step at n = 200: 336 for 314
 // useful (93%; the staged kernel's 16 x 16 super-tiles: 384).
 #ifndef TSNMF_GC_L1PF
-#define TSNMF_GC_L1PF 0
+#define TSNMF_GC_L1PF 0  // L1 prefetch of the next k-step's lines: 8 warps 1157 -> 1094 GB/s, 12 warps 974 -> 1075 (off)
 #endif
 constexpr int kGcAhead = 8;  // L2 prefetch distance in k-steps (4 rows each)
 

@@ -331,6 +331,32 @@ def test_gram_narrow_every_width(n, monkeypatch):
         monkeypatch.delenv(var)
 
 
+@pytest.mark.parametrize("n", list(range(193, 201)))
+def test_gram_cyclic_widths(n, monkeypatch):
+    """Cyclic register Gram (25 tile columns, n = 193..200): both warp layouts and the staged kernel against
+    numpy on ragged row counts and a strided view; the last tile column is partial below n = 200."""
+    rng = np.random.default_rng(300 + n)
+    wide = rng.standard_normal((30_011, 210)) * np.logspace(0, -2, 210)
+    for variant in (None, "8", "12", "0"):
+        if variant is None:
+            monkeypatch.delenv("TSNMF_GRAM_CYCLIC", raising=False)
+        else:
+            monkeypatch.setenv("TSNMF_GRAM_CYCLIC", variant)
+        for m in (1, 6, 1021, 30_011):
+            x = np.ascontiguousarray(wide[:m, :n])
+            g, l1, sq = dv.gram(dev(x))
+            assert rel_err(g.cpu().numpy(), x.T @ x) <= 1e-13, (variant, n, m)
+            assert np.abs(g.cpu().numpy() - x.T @ x).max() <= 1e-13 * np.abs(x.T @ x).max()
+            assert np.array_equal(g.cpu().numpy(), g.cpu().numpy().T)
+            np.testing.assert_allclose(l1.cpu().numpy(), np.abs(x).sum(0), rtol=1e-12)
+            np.testing.assert_allclose(sq.cpu().numpy(), (x * x).sum(0), rtol=1e-12)
+        view = dev(wide)[:, 7:7 + n]
+        want = wide[:, 7:7 + n].T @ wide[:, 7:7 + n]
+        got = dv.gram(view)[0].cpu().numpy()
+        assert rel_err(got, want) <= 1e-13, (variant, n, "strided")
+        assert np.array_equal(got, dv.gram(view)[0].cpu().numpy())
+
+
 def test_gram_equivalence_invariant():
     """‖RᵀR − XᵀX‖_F ≤ 1e-10 ‖XᵀX‖_F (reference SPEC.md:164) on the device outputs."""
     x = np.random.default_rng(11).uniform(0, 1, (100_000, 50))
