@@ -10,6 +10,7 @@ The text format is not mirrored.
 
 from __future__ import annotations
 
+import os
 import struct
 from pathlib import Path
 
@@ -99,10 +100,16 @@ class ChunkReader:
     and yielded as row views of the batch, so ``stream_pass`` reduces consecutive chunks as one batch.
     Chunk boundaries, order, counters, hash and error positions are those of the host reader: chunks
     before a non-finite entry are yielded, the error is raised when its chunk is reached.
+
+    ``gds`` (new, device mode only): read the batches with cuFile (GPUDirect Storage, ``gds.py``) straight
+    into device batches, a read-ahead thread issuing the next ``cuFileRead`` while the current batch is
+    consumed; no host copy of the payload exists, so it applies when no ``hasher`` is given
+    (the content hash is defined over host bytes; a hashed run keeps the pinned-buffer path).  ``None``
+    follows the environment (``TSNMF_GDS=1``); ``True`` raises ``TsnmfError`` when libcufile is missing.
     """
 
     def __init__(self, path, chunk_rows: int = DEFAULT_CHUNK_ROWS, *, validate: bool = True, hasher=None,
-                 device=None, batch_bytes: int = 1 << 30):
+                 device=None, batch_bytes: int = 1 << 30, gds: bool | None = None):
         if chunk_rows < 1:
             raise UsageError(f"chunk_rows must be >= 1, got {chunk_rows}")
         self.path = Path(path)
@@ -111,6 +118,9 @@ class ChunkReader:
         self.hasher = hasher
         self.device = device
         self.batch_bytes = int(batch_bytes)
+        if gds and device is None:
+            raise UsageError("gds=True needs device= (cuFile reads into device memory)")
+        self.gds = gds
         self.rows_read = 0
         self.bytes_read = 0
         size = self.path.stat().st_size
@@ -134,6 +144,9 @@ class ChunkReader:
     def __iter__(self):
         if self.device is None:
             return self._iter_host()
+        gds = self.gds if self.gds is not None else os.environ.get("TSNMF_GDS", "0") not in ("", "0")
+        if gds and self.hasher is None:
+            return self._iter_device_gds()
         return self._iter_device()
 
     def _read_header(self, f) -> None:
@@ -220,6 +233,64 @@ class ChunkReader:
                     if self.hasher is not None:
                         self.hasher.update(raw)
                     self.bytes_read += len(raw)
+                    if bad >= 0 and r0 + c > good_rows:
+                        raise _nonfinite_error(offset + r0, good_rows - r0, int(bad % n))
+                    self.rows_read += c
+                    yield RowChunk(row_offset=offset + r0, data=xb[r0:r0 + c])
+
+    def _iter_device_gds(self):
+        """cuFile path: file -> device batches without a host copy (see the class docstring)."""
+        from concurrent.futures import ThreadPoolExecutor
+
+        from . import device as dv
+        from . import gds
+
+        t = dv.torch()
+        dev = t.device(self.device) if not isinstance(self.device, int) else t.device("cuda", self.device)
+        if dev.type != "cuda":
+            raise UsageError(f"ChunkReader device must be a CUDA device, got {self.device!r}")
+        if dev.index is None:
+            dev = t.device("cuda", t.cuda.current_device())
+        n = self._cols
+        row_bytes = n * 8
+        per_batch = max(1, self.batch_bytes // (row_bytes * self.chunk_rows)) * self.chunk_rows
+        per_batch = min(per_batch, max(self._rows, 1))
+        batches = [(o, min(per_batch, self._rows - o)) for o in range(0, self._rows, per_batch)]
+        compute = t.cuda.current_stream(dev)
+        self.bytes_read += HEADER_BYTES  # the header was read (and checked) by the constructor
+        with gds.FileHandle(self.path) as fh, ThreadPoolExecutor(max_workers=1) as pool:
+
+            def read_into(xb, ready, offset, rows):  # worker thread: blocking cuFileRead into a device batch
+                # cuFileRead is not stream-ordered: the batch's memory may be a block the caching allocator
+                # took back from an earlier batch whose kernels are still running on the consumer's stream
+                ready.synchronize()
+                with t.cuda.device(dev):
+                    return fh.read_into(xb.data_ptr(), rows * row_bytes, HEADER_BYTES + offset * row_bytes)
+
+            def submit(offset, rows):
+                # a fresh device batch per read (the consumer keeps views of earlier batches until it has
+                # launched their reduction); the read of batch i + 2 so overlaps the reduction of batch i
+                with t.cuda.device(dev):
+                    xb = t.empty((rows, n), dtype=t.float64, device=dev)
+                    ready = t.cuda.Event()
+                    ready.record(compute)
+                return xb, pool.submit(read_into, xb, ready, offset, rows)
+
+            nxt = submit(*batches[0]) if batches else None
+            for i, (offset, rows) in enumerate(batches):
+                xb, fut = nxt
+                got = fut.result()
+                nxt = submit(*batches[i + 1]) if i + 1 < len(batches) else None
+                if got < rows * row_bytes:
+                    whole = got // (self.chunk_rows * row_bytes) * self.chunk_rows
+                    self.rows_read += whole
+                    self.bytes_read += whole * row_bytes
+                    raise DataError("payload shorter than declared")
+                bad = dv.first_nonfinite(xb) if self.validate else -1
+                good_rows = rows if bad < 0 else (bad // n)
+                for r0 in range(0, rows, self.chunk_rows):
+                    c = min(self.chunk_rows, rows - r0)
+                    self.bytes_read += c * row_bytes
                     if bad >= 0 and r0 + c > good_rows:
                         raise _nonfinite_error(offset + r0, good_rows - r0, int(bad % n))
                     self.rows_read += c

@@ -33,11 +33,17 @@ for ch in rd:
     pass
 torch.cuda.synchronize(); t_rd = time.perf_counter() - t0
 print(f"reader alone: {gb / t_rd:6.2f} GB/s ({t_rd:.2f} s incl. {t_init:.2f} s setup)", flush=True)
-for label, dev in (("device", "cuda"), ("host chunks", None)):
+from paper_1402_6964_b200 import gds
+cases = [("device", dict(device="cuda")), ("host chunks", dict())]
+if gds.available():
+    cases.insert(1, ("device, cuFile", dict(device="cuda", gds=True)))
+for label, kw in cases:
+    if kw.get("gds"):
+        tb.stream_pass(tb.ChunkReader(path, **kw))  # first use opens the cuFile driver (not timed)
     torch.cuda.synchronize(); t0 = time.perf_counter()
-    res = tb.stream_pass(tb.ChunkReader(path, device=dev))
+    res = tb.stream_pass(tb.ChunkReader(path, **kw))
     torch.cuda.synchronize(); t = time.perf_counter() - t0
-    print(f"{label:12s}: {gb / t:6.2f} GB/s ({t:.2f} s, rows {res.rows}, chunks {res.chunks})", flush=True)
+    print(f"{label:14s}: {gb / t:6.2f} GB/s ({t:.2f} s, rows {res.rows}, chunks {res.chunks})", flush=True)
 print(f"raw sequential read {gb / t_read:.2f} GB/s; device finiteness scan {gb / t_scan:.0f} GB/s "
       f"({m} x {n}, {gb:.1f} GB)")
 os.remove(path)
