@@ -37,6 +37,12 @@ int tsqr_run(const double* x, int64_t m, int n, int64_t ldx, double* r, int64_t 
 int r_combine_run(const double* rs, int count, int n, double* r, int64_t ldr, void* ws, size_t ws_bytes,
                   cudaStream_t st);
 int tsqr_describe(int n, int64_t m, int* nb, int* brows, int* ctas_per_sm, int* nleaves);
+// register-block leaf with DMMA trailing updates (tsqr_reg.cu)
+bool tsqr_reg_supported(int n);
+int tsqr_reg_block_rows(int n);
+int tsqr_reg_warps_per_cta();
+int tsqr_reg_leaf_run(const double* x, int64_t m, int64_t ldx, int n, int64_t rpw, int nleaves, int npad,
+                      double* slots, double* stats, cudaStream_t st);
 
 size_t nnls_workspace_bytes(int t);
 int nnls_max_design_cols();

@@ -936,7 +936,10 @@ __device__ __noinline__ void update_global(const double* __restrict__ Bs, int ld
 #ifndef TSNMF_SPLIT_PREFETCH
 #define TSNMF_SPLIT_PREFETCH 0  // measured: none 265, at block start 261, late 261 GB/s (C2 shape, 2^24 rows)
 #endif
-constexpr int kSplitPrefetch = TSNMF_SPLIT_PREFETCH;  // next block's right columns into L2: 0 off, 1 at block start, 2 late
+constexpr int kSplitPrefetch = TSNMF_SPLIT_PREFETCH;
+#ifndef TSNMF_TSQR_REGLEAF_DEFAULT
+#define TSNMF_TSQR_REGLEAF_DEFAULT 1
+#endif  // next block's right columns into L2: 0 off, 1 at block start, 2 late
 // L2 prefetch of the right columns [lcols, ncols) of rows [row0, row0 + 256) (their first updates read X)
 __device__ __forceinline__ void prefetch_next_right(const double* X, int64_t ldx, int64_t nrows, int64_t row0,
                                                     int lcols, int ncols, int t, int nt) {
@@ -1913,6 +1916,24 @@ int split_leaf(const double* x, int64_t m, int64_t ldx, const SplitGeom& sg, int
   return kOk;
 }
 
+// Register-block leaf with DMMA trailing updates (tsqr_reg.cu, widths 25..64): the default for 28 <= n <= 64
+// (measured against the older leaves at 2^25 rows, tools/reg_leaf_sweep.py: n = 28 866 vs 783 GB/s, n = 32 872 vs
+// 639, n = 40 785 vs 521, n = 48 592 vs 515, n = 64 497 vs 434; n = 25..27 stay with the exact-width warp leaf,
+// n = 25 814 vs 1146).  TSNMF_TSQR_REGLEAF=1/0 forces it / the older leaves.
+bool reg_leaf_path(int n) {
+  if (!tsqr_reg_supported(n)) return false;
+  if (const char* e = getenv("TSNMF_TSQR_REGLEAF")) return atoi(e) != 0;
+  return TSNMF_TSQR_REGLEAF_DEFAULT != 0 && n >= 28;
+}
+void reg_leaf_plan(int n, int64_t m, int* nleaves, int64_t* rows_per_warp) {
+  const int64_t br = tsqr_reg_block_rows(n);
+  const int64_t max_leaves = (int64_t)device_sms() * tsqr_reg_warps_per_cta();
+  const int64_t leaves = max64(1, min64(max_leaves, ceil_div(m, br)));
+  const int64_t rpw = round_up(ceil_div(m, leaves), br);
+  *nleaves = (int)ceil_div(m, rpw);
+  *rows_per_warp = rpw;
+}
+
 }  // namespace
 
 int tsqr_max_cols() { return 512; }
@@ -1934,7 +1955,9 @@ size_t tsqr_workspace_bytes(int64_t m, int n) {
   int nleaves;
   int64_t rpc;
   size_t extra = 0;
-  if (small_path(n)) {
+  if (reg_leaf_path(n)) {
+    reg_leaf_plan(n, max64(m, 1), &nleaves, &rpc);
+  } else if (small_path(n)) {
     narrow_plan(n, max64(m, 1), &nleaves, &rpc);
   } else if (split_path(n)) {
     split_plan(n, max64(m, 1), &nleaves, &rpc);
@@ -1959,10 +1982,13 @@ int tsqr_run(const double* x, int64_t m, int n, int64_t ldx, double* r, int64_t 
   if (!tq_config(n, &ch)) return set_error(kUsage, "tsqr: n = %d columns does not fit the on-chip block", n);
   int nleaves;
   int64_t rpc;
-  const bool narrow = small_path(n);
-  const bool split = !narrow && split_path(n);
+  const bool reg = reg_leaf_path(n);
+  const bool narrow = !reg && small_path(n);
+  const bool split = !reg && !narrow && split_path(n);
   size_t extra = 0;
-  if (narrow) {
+  if (reg) {
+    reg_leaf_plan(n, m, &nleaves, &rpc);
+  } else if (narrow) {
     narrow_plan(n, m, &nleaves, &rpc);
   } else if (split) {
     split_plan(n, m, &nleaves, &rpc);
@@ -1977,7 +2003,15 @@ int tsqr_run(const double* x, int64_t m, int n, int64_t ldx, double* r, int64_t 
   double* stats = slots + (int64_t)nleaves * npad * npad;
   const bool want_stats = (l1 != nullptr) || (sumsq != nullptr);
   int rc;
-  if (narrow && warp_leaf_path(n)) {
+  if (reg) {
+    rc = tsqr_reg_leaf_run(x, m, ldx, n, rpc, nleaves, (int)npad, slots, want_stats ? stats : nullptr, st);
+    if (!rc) {
+      if (n <= 32)
+        rc = n <= 28 ? small_tree<28>(n, nleaves, (int)npad, slots, st) : small_tree<32>(n, nleaves, (int)npad, slots, st);
+      else
+        rc = tq_dispatch(ch, nullptr, 0, 0, slots, nullptr, nleaves, 0, st);
+    }
+  } else if (narrow && warp_leaf_path(n)) {
     rc = warp_leaf(x, m, n, ldx, rpc, nleaves, slots, want_stats ? stats : nullptr, st);
   } else if (narrow) {
     rc = small_leaf(x, m, n, ldx, rpc, nleaves, (int)npad, slots, want_stats ? stats : nullptr, st);
@@ -2019,6 +2053,13 @@ int tsqr_describe(int n, int64_t m, int* nb, int* brows, int* ctas_per_sm, int* 
   TqChoice ch;
   if (!tq_config(n, &ch)) return set_error(kUsage, "tsqr: n = %d too large", n);
   int64_t rpc;
+  if (reg_leaf_path(n)) {  // register-block leaf with DMMA trailing updates: one warp per leaf
+    reg_leaf_plan(n, max64(m, 1), nleaves, &rpc);
+    *nb = kNB;
+    *brows = tsqr_reg_block_rows(n);
+    *ctas_per_sm = 1;
+    return kOk;
+  }
   if (warp_leaf_path(n)) {  // register-block warp leaf: "panel" 1 column, 32*S-row blocks, one warp per CTA
     warp_leaf_plan(n, max64(m, 1), nleaves, &rpc);
     const int S = warp_leaf_s(n);

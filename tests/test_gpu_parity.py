@@ -162,7 +162,9 @@ def test_tall_shapes_and_tree_edges(oracle, m):
                                  (1, 5000), (2, 4099), (24, 300_001), (31, 65_537)])
 def test_narrow_warp_chain_path(oracle, monkeypatch, n, m):
     """n <= 32 runs one Householder chain per warp (many leaves, warp-level combine tree with leftover
-    folds, partial 32-row blocks); it must agree with the oracle and with the shared-panel path."""
+    folds, partial 32-row blocks); it must agree with the oracle and with the shared-panel path.  (28 <= n <= 32
+    default to the register-block DMMA leaf, test_register_leaf_matches_oracle; it is switched off here.)"""
+    monkeypatch.setenv("TSNMF_TSQR_REGLEAF", "0")
     rng = np.random.default_rng(n * 7 + m)
     x = rng.uniform(-1, 1, (m, n)) * np.logspace(0, -3, n)
     xd = dev(x)
@@ -304,6 +306,39 @@ def test_gram_matches_numpy(n):
     assert np.array_equal(g.gram, g.gram.T)
     np.testing.assert_allclose(g.stats.l1, np.abs(x).sum(0), rtol=1e-12)
     np.testing.assert_allclose(g.stats.l2, np.linalg.norm(x, axis=0), rtol=1e-12)
+
+
+@pytest.mark.parametrize("n", [25, 28, 31, 32, 33, 40, 41, 48, 49, 56, 57, 63, 64])
+def test_register_leaf_matches_oracle(n, oracle, monkeypatch):
+    """Register-block TSQR leaf with DMMA trailing updates (tsqr_reg.cu; default for 28 <= n <= 64, forced here
+    for 25): one row, fewer rows than a block, ragged multi-leaf row counts, a strided view, zero / duplicate
+    columns (non-unique R: compared through R^T R), and the older leaves on the same input."""
+    monkeypatch.delenv("TSNMF_TSQR_REGLEAF", raising=False)
+    plan = dv.tsqr_plan(n, 1 << 20)
+    assert (plan["panel"] == 8 and plan["block_rows"] in (48, 64, 72, 80)) == (n >= 28)  # the default from n = 28 up
+    monkeypatch.setenv("TSNMF_TSQR_REGLEAF", "1")
+    rng = np.random.default_rng(500 + n)
+    for m in (n, n + 3, 1000, 70_001):
+        x = rng.standard_normal((m, n)) * np.logspace(0, -3, n)
+        r, l1, sq = dv.tsqr(dev(x))
+        r = r.cpu().numpy()
+        assert rel_err(r, oracle.factor_chunk(x)) <= R_TOL, (n, m)
+        assert np.all(np.tril(r, -1) == 0) and np.all(np.diagonal(r) >= 0)
+        np.testing.assert_allclose(l1.cpu().numpy(), np.abs(x).sum(0), rtol=1e-12)
+        np.testing.assert_allclose(sq.cpu().numpy(), (x * x).sum(0), rtol=1e-12)
+    wide = rng.uniform(0, 1, (40_000, 80))
+    view = dev(wide)[:, 9:9 + n]
+    got = dv.tsqr(view)[0].cpu().numpy()
+    assert rel_err(got, oracle.factor_chunk(np.ascontiguousarray(wide[:, 9:9 + n]))) <= R_TOL
+    assert np.array_equal(got, dv.tsqr(view)[0].cpu().numpy())  # bitwise repeatable
+    monkeypatch.setenv("TSNMF_TSQR_REGLEAF", "0")
+    assert rel_err(dv.tsqr(view)[0].cpu().numpy(), got) <= 1e-12
+    monkeypatch.setenv("TSNMF_TSQR_REGLEAF", "1")
+    x = rng.uniform(0, 1, (20_000, n))
+    x[:, 2] = 0.0
+    x[:, n - 1] = x[:, 0]
+    r = dv.tsqr(dev(x))[0].cpu().numpy()
+    assert rel_err(r.T @ r, x.T @ x) <= 1e-12
 
 
 @pytest.mark.parametrize("n", list(range(1, 65)))
