@@ -484,7 +484,7 @@ def main():
     plan = dv.tsqr_plan(n, hi - lo)
     narrow = plan["panel"] == 1  # n <= 32: register-block warp leaf (FP64 FMA), else the DMMA panel leaf
     # the committed ncu captures are per width: traffic is only reported for a width one was taken at
-    captures = {25: ("r01_tsqr_warp_leaf_ncu_full.txt", 1 << 22), 64: ("r02_tsqr_leaf_n64_ncu_full.txt", 1 << 21),
+    captures = {25: ("r02_tsqr_warp_leaf_ncu_full.txt", 1 << 22), 64: ("r02_tsqr_reg_leaf_n64_ncu_full.txt", 1 << 21),
                 200: (TSQR_N200_CAPTURE, 1 << 21)}
     prof_file, prof_rows = captures.get(n, ("(none)", 0))
     prof_n = n if n in captures else None
@@ -511,6 +511,8 @@ def main():
                      "kernel": ("tsqr_warp_leaf_kernel (FP64 FMA, one Householder chain per warp)" if narrow
                                 else "tsqr_split_leaf_kernel (FP64 DMMA m8n8k4; 256-row blocks, right column "
                                      "tiles in an L2 workspace)" if plan["block_rows"] == 256
+                                else "tsqr_reg_leaf_kernel (one Householder chain per warp, row block in registers, "
+                                     "FP64 DMMA m8n8k4 trailing updates)" if 28 <= n <= 64 and plan["ctas_per_sm"] == 1
                                 else "tsqr_leaf_kernel (FP64 DMMA m8n8k4)"),
                      "algorithmic": f"2 n^2 = {2 * n * n} flop per row x {hi - lo} rows per launch",
                      "peak_source": ("measured FP64 DFMA peak" if narrow else "measured FP64 DMMA peak")
