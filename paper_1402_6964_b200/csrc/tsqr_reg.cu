@@ -28,6 +28,9 @@
 namespace tsnmf {
 
 constexpr int kRgWarps = 8;
+#ifndef TSNMF_RG_SCALE_FROM_TAU
+#define TSNMF_RG_SCALE_FROM_TAU 1
+#endif
 
 template <int TCN, int NT>
 struct RgLayout {
@@ -173,14 +176,29 @@ __global__ void __launch_bounds__(32 * kRgWarps, 1)
           const double rjc = Rd[j * 8 + cj];
           const bool live = sigma > 0.0;
           const double ss = live ? fma(alpha, alpha, sigma) : 1.0;
+// (rsqrt_nb's range scaling stays: a uniform fast-path branch around it splits the step's basic block and
+          // costs far more than the three multiplies it saves — n = 40 804 -> 625 GB/s)
           const double inv = rsqrt_nb(ss);
           const double nrm = ss * inv;
           const double beta = live ? -copysign(nrm, alpha) : alpha;
           const double tau = live ? fma(fabs(alpha), inv, 1.0) : 0.0;
+#if TSNMF_RG_SCALE_FROM_TAU
+          // 1 / (|alpha| + nrm) = inv / tau with tau in [1, 2]: the reciprocal needs no range scaling and starts
+          // from inv, not from nrm
+          double rt;
+          asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rt) : "d"(tau));
+          rt = rt * fma(-tau, rt, 2.0);
+          rt = rt * fma(-tau, rt, 2.0);
+          const double scale = live ? copysign(inv * rt, alpha) : 0.0;
+#else
           const double scale = live ? copysign(rcp_nb(fabs(alpha) + nrm), alpha) : 0.0;
+#endif
           const double tw = tau * fma(scale, d, rjc);
           const double f = cj > j ? tw * scale : 0.0;
-          if (cj > j) {
+          // straight-line, predicated (f = 0 for the finished and the pivot columns): a divergent branch here
+          // would split the step's basic block, which the scheduler needs whole to hide the scalar chain
+          {
+            const bool nxt = cj == j + 1;
 #pragma unroll
             for (int t = 0; t < NT; ++t) {
               double2 v;
@@ -190,14 +208,11 @@ __global__ void __launch_bounds__(32 * kRgWarps, 1)
                 v = *reinterpret_cast<const double2*>(xcur + 8 * t + 2 * kr);
               B[t][0][Tp] = fma(-f, v.x, B[t][0][Tp]);
               B[t][1][Tp] = fma(-f, v.y, B[t][1][Tp]);
-              if (cj == j + 1)
+              if (nxt)
                 *reinterpret_cast<double2*>(XC + (j + 1) * BRS + 8 * t + 2 * kr) = make_double2(B[t][0][Tp], B[t][1][Tp]);
             }
-            if (kr == 0) Rd[j * 8 + cj] = rjc - tw;
-          }
-          if (cj == j) {
-            myscale = scale;
-            if (kr == 0) Rd[j * 8 + j] = beta;
+            if (kr == 0 && cj >= j) Rd[j * 8 + cj] = cj == j ? beta : rjc - tw;
+            myscale = cj == j ? scale : myscale;
           }
           trow[j] = lane == j ? tau : (lane < j ? -tau * scale * tacc : 0.0);
         }
