@@ -39,8 +39,8 @@ struct RgLayout {
   static constexpr int BRS = BR + (20 - BR % 16) % 16;    // column stride of XC, = 4 (mod 16): conflict-free V^T reads
   static constexpr int r_off = 0;
   static constexpr int x_off = r_off + NTILES * 64;       // XC: the panel's 8 pivot columns as broadcast (unscaled)
-  static constexpr int w_off = x_off + 8 * BRS;           // W / W' scratch tile (8 x 8)
-  static constexpr int t_off = w_off + 64;                // T (8 x 8, row r = reflector r)
+  static constexpr int w_off = x_off + 8 * BRS;           // W / W' scratch tiles (2 x 8 x 8: two trailing tiles per round)
+  static constexpr int t_off = w_off + 128;               // T (8 x 8, row r = reflector r)
   static constexpr int d_off = t_off + 64;                // the step's dots (8)
   static constexpr int total = d_off + 8;
   static constexpr size_t bytes = sizeof(double) * (size_t)total * kRgWarps;
@@ -222,39 +222,65 @@ __global__ void __launch_bounds__(32 * kRgWarps, 1)
         for (int c = 0; c < 8; ++c) Tm[lane * 8 + c] = trow[c];
       }
       __syncwarp();
-      // ---- trailing column tiles: W = R_p + D Xc^T B; W' = T^T W; R_p -= W'; B -= Xc (D W')
+      // ---- trailing column tiles: W = R_p + D Xc^T B; W' = T^T W; R_p -= W'; B -= Xc (D W').  Two tiles per
+      // round (independent DMMA chains, one set of warp barriers and one set of V^T fragment loads for both).
 #pragma unroll
-      for (int Tc = Tp + 1; Tc < TCN; ++Tc) {
+      for (int Tc = Tp + 1; Tc < TCN; Tc += 2) {
         if (8 * Tc >= n) break;
+        const bool two = Tc + 1 < TCN;  // (TCN = ceil(n / 8): every tile column below TCN holds real columns)
+        const int Td = Tc + 1 < TCN ? Tc + 1 : Tc;  // second tile (static index; == Tc when there is none)
         double* Rp = Rt + rg_tile(TCN, Tp, Tc) * 64;
+        double* Rq = Rt + rg_tile(TCN, Tp, Td) * 64;
+        double* Wsd = Wsc + 64;
         const double2 rinit = *reinterpret_cast<const double2*>(Rp + ci);
-        double a00 = 0.0, a01 = 0.0, a10 = 0.0, a11 = 0.0;
+        const double2 qinit = *reinterpret_cast<const double2*>(Rq + ci);
+        double a00 = 0.0, a01 = 0.0, a10 = 0.0, a11 = 0.0, b00 = 0.0, b01 = 0.0, b10 = 0.0, b11 = 0.0;
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
           dmma(a00, a01, B[t][0][Tp], B[t][0][Tc]);
           dmma(a10, a11, B[t][1][Tp], B[t][1][Tc]);
+          if (two) {
+            dmma(b00, b01, B[t][0][Tp], B[t][0][Td]);
+            dmma(b10, b11, B[t][1][Tp], B[t][1][Td]);
+          }
         }
         Wsc[ci] = fma(myscale, a00 + a10, rinit.x);  // this lane's tile row i = cj: its own group's scale
         Wsc[ci + 1] = fma(myscale, a01 + a11, rinit.y);
+        if (two) {
+          Wsd[ci] = fma(myscale, b00 + b10, qinit.x);
+          Wsd[ci + 1] = fma(myscale, b01 + b11, qinit.y);
+        }
         __syncwarp();
-        double w0 = 0.0, w1 = 0.0;
+        double w0 = 0.0, w1 = 0.0, u0 = 0.0, u1 = 0.0;
 #pragma unroll
-        for (int k0 = 0; k0 < 8; k0 += 4)
-          dmma(w0, w1, Tm[(k0 + (lane & 3)) * 8 + (lane >> 2)], Wsc[(k0 + (lane & 3)) * 8 + (lane >> 2)]);
+        for (int k0 = 0; k0 < 8; k0 += 4) {
+          const double tf = Tm[(k0 + (lane & 3)) * 8 + (lane >> 2)];
+          dmma(w0, w1, tf, Wsc[(k0 + (lane & 3)) * 8 + (lane >> 2)]);
+          if (two) dmma(u0, u1, tf, Wsd[(k0 + (lane & 3)) * 8 + (lane >> 2)]);
+        }
         *reinterpret_cast<double2*>(Rp + ci) = make_double2(rinit.x - w0, rinit.y - w1);
+        if (two) *reinterpret_cast<double2*>(Rq + ci) = make_double2(qinit.x - u0, qinit.y - u1);
         __syncwarp();
         Wsc[ci] = w0 * myscale;
         Wsc[ci + 1] = w1 * myscale;
+        if (two) {
+          Wsd[ci] = u0 * myscale;
+          Wsd[ci + 1] = u1 * myscale;
+        }
         __syncwarp();
         const double wb0 = -Wsc[(lane & 3) * 8 + (lane >> 2)];
         const double wb1 = -Wsc[(4 + (lane & 3)) * 8 + (lane >> 2)];
+        const double wd0 = two ? -Wsd[(lane & 3) * 8 + (lane >> 2)] : 0.0;
+        const double wd1 = two ? -Wsd[(4 + (lane & 3)) * 8 + (lane >> 2)] : 0.0;
         __syncwarp();
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
           const double v0 = XC[(lane & 3) * BRS + 8 * t + (lane >> 2)];
           const double v1 = XC[(4 + (lane & 3)) * BRS + 8 * t + (lane >> 2)];
           dmma(B[t][0][Tc], B[t][1][Tc], wb0, v0);
+          if (two) dmma(B[t][0][Td], B[t][1][Td], wd0, v0);
           dmma(B[t][0][Tc], B[t][1][Tc], wb1, v1);
+          if (two) dmma(B[t][0][Td], B[t][1][Td], wd1, v1);
         }
       }
     }
