@@ -531,7 +531,14 @@ def main():
         line["gram"] = {"value": bytes_total / (gms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": gms,
                         "kernel_ms": gk_ms, "kernel_tflops": gflops / (gk_ms * 1e-3) / 1e12,
                         "frac_fp64": gflops / (gk_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
-                        "hbm_frac": bytes_local / (gk_ms * 1e-3) / 1e9 / hbm}
+                        "hbm_frac": bytes_local / (gk_ms * 1e-3) / 1e9 / hbm,
+                        "kernel": ("gram_narrow_kernel (fragments from global memory, upper triangle in each warp's "
+                                   "registers)" if n <= 64 else
+                                   "gram_cyclic_kernel (25 tile columns, every tile pair once, accumulators in "
+                                   "registers)" if 193 <= n <= 200 else "gram_kernel (staged, 16x16 super-tiles)"),
+                        "ncu": {25: "profiles/r02_gram_narrow_n25_ncu_full.txt",
+                                64: "profiles/r02_gram_narrow_n64_ncu_full.txt",
+                                200: "profiles/r02_gram_cyclic_ncu_full.txt"}.get(n)}
         # size-independent full-m checks of this pass (parity against the oracle at full m is
         # tests/parity_full.py -> profiles/r02_parity_full.json): R^T R = X^T X with X^T X from
         # the independent Gram kernel, R upper triangular with a nonnegative diagonal
